@@ -1,0 +1,146 @@
+/* gwas.h -- C-ABI of the B200-native CLAK-Eig hot path (libgwas.so).
+ *
+ * The library solves the 2-D sequence of generalised least-squares problems of PAPER.md Eq. probDef
+ * (P:26-40): for every SNP i (1..m) and trait j (1..t), with X_i = [X_L | g_i] (n x w, w = p + 1),
+ *
+ *     b_ij   = (X_i^T M_j^-1 X_i)^-1 X_i^T M_j^-1 y_j,     M_j = sigma2_j (h2_j Phi + (1 - h2_j) I)
+ *     Var_ij = (X_i^T M_j^-1 X_i)^-1                       (var_convention 0; reading A1)
+ *            = sigma2_j (X_i^T M_j^-1 X_i)^-1              (var_convention 1; P:31 as printed)
+ *
+ * by CLAK-Eig for multi-trait analysis (Alg. 4):
+ *     gwas_setup  = Alg. 4 lines 1, 2, 4 and the per-trait block 6-11: Phi = Z W Z^T
+ *                   (cuSOLVER dsyevd, timed separately), X_L' = Z^T X_L, Y' = Z^T Y, D_j, and the
+ *                   Cholesky-factored top-left blocks S_TL_j = X_L'^T D_j X_L', b_T_j = X_L'^T D_j y'_j;
+ *     gwas_run    = Alg. 4 line 3 (X_R := Z^T X_R) streamed in column blocks, and the inner loop
+ *                   lines 13-16 for every (i, j) of the block.
+ *
+ * Conventions (all calls):
+ *   - Matrices are column-major fp64 unless stated; sizes are int64_t; "ld" = leading dimension in elements.
+ *   - The caller owns every buffer (state, workspace, outputs) and every stream; the library allocates no
+ *     device memory (a cuSOLVER handle is created inside gwas_setup only).
+ *   - Pointers documented "host or device" are classified with cudaPointerGetAttributes.
+ *   - Calls enqueue on options.compute_stream (and options.copy_stream for staging) and return without
+ *     synchronising, except gwas_setup / gwas_attach, which synchronise to report errors.
+ *   - On error a call returns a non-zero gwas_status and gwas_last_error() (thread-local) names the cause
+ *     (for GWAS_E_NOT_SPD: the trait j and, for D_j, the eigen-index k).
+ *   - Per-pair numerical failures never fail a call: status[i][j] = 1 (SNP collinear with X_L: Schur
+ *     complement sigma_ij <= eps_collinear * c_ij, reading A6) or 2 (non-finite), with NaN payload.
+ */
+#ifndef GWAS_H
+#define GWAS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GWAS_API __attribute__((visibility("default")))
+#else
+#define GWAS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gwas_ctx gwas_ctx; /* opaque, bound to one CUDA device */
+
+typedef enum {
+  GWAS_OK = 0,
+  GWAS_E_ARG = 1,      /* bad pointer / shape / range: n < p + 1, p < 1, t < 1, h2 outside [0,1], sigma2 <= 0,
+                          non-finite inputs, unaligned ld, unpinned host X_R, ... */
+  GWAS_E_NOT_SPD = 2,  /* some sigma2_j (h2_j w_k + 1 - h2_j) <= eps_spd (reading A7), or S_TL_j not SPD
+                          (X_L rank-deficient); message names j (and k) */
+  GWAS_E_EIG = 3,      /* cusolverDnDsyevd reported info != 0 */
+  GWAS_E_CUDA = 4,     /* a CUDA / cuSOLVER runtime error */
+  GWAS_E_NOMEM = 5,    /* caller-provided state or workspace smaller than gwas_state_bytes / _workspace_bytes */
+  GWAS_E_STATE = 6     /* wrong call order, or a state buffer whose header does not match (gwas_attach) */
+} gwas_status;
+
+enum { GWAS_XR_F64 = 0, GWAS_XR_U8 = 1 };          /* X_R element type: fp64, or uint8 dosages (exact) */
+enum { GWAS_OUT_SNP = 0, GWAS_OUT_FULL = 1 };      /* outputs per pair: (b_g, Var_gg) or w entries of b, diag Var */
+enum { GWAS_VAR_TEXTBOOK = 0, GWAS_VAR_LITERAL = 1 };
+enum { GWAS_PAIR_OK = 0, GWAS_PAIR_COLLINEAR = 1, GWAS_PAIR_NONFINITE = 2 };
+enum { GWAS_K1 = 0, GWAS_K2 = 1, GWAS_K3 = 2, GWAS_H2D = 3, GWAS_NUM_TIMERS = 4 };
+
+typedef struct {
+  int32_t device;          /* CUDA ordinal the context binds to */
+  int32_t xr_dtype;        /* GWAS_XR_F64 or GWAS_XR_U8 */
+  int32_t output_mode;     /* GWAS_OUT_SNP (default) or GWAS_OUT_FULL */
+  int32_t var_convention;  /* GWAS_VAR_TEXTBOOK (default) or GWAS_VAR_LITERAL */
+  int64_t block_cols;      /* SNP columns per streamed block k ("user-configurable"); default 8192 */
+  double eps_spd;          /* default 1e-10 */
+  double eps_collinear;    /* default 1e-10, relative Schur-complement threshold (reading A6) */
+  void* compute_stream;    /* cudaStream_t for kernels (NULL = legacy default stream) */
+  void* copy_stream;       /* cudaStream_t for host->HBM staging of X_R blocks (NULL = compute_stream) */
+  int32_t timing;          /* 1 = bracket every K1/K2/K3/H2D launch with CUDA events (gwas_kernel_times) */
+  int32_t reserved;
+} gwas_options;
+
+/* Fills the defaults listed above (device 0, u8 X_R). */
+GWAS_API void gwas_default_options(gwas_options* opt);
+
+/* Bytes of the replicated state buffer (header + Z + W + B_op/D operand + per-trait factors).  The buffer is
+ * position-independent: rank 0 fills it in gwas_setup, other ranks receive it byte-for-byte (one NCCL
+ * broadcast) and call gwas_attach.  Returns 0 on invalid sizes. */
+GWAS_API size_t gwas_state_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* opt);
+
+/* Bytes of per-device scratch: max(setup needs incl. the dsyevd workspace, run needs = 2 staging buffers +
+ * the rotated block X_R' + the block's reductions).  Queries cuSOLVER on opt->device.  0 on error. */
+GWAS_API size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* opt);
+
+/* Alg. 4 lines 1-2, 4, 6-11.
+ *   phi    n x n symmetric (col-major, ld = n), host or device, read-only
+ *   XL     n x p (col-major, ld = n), column 0 is the intercept (any full-column-rank X_L is accepted)
+ *   Y      n x t (col-major, ld = n)
+ *   h2, sigma2   t values each (host or device); h2 in [0,1], sigma2 > 0
+ *   state_dev / work_dev   caller-owned device buffers of at least the sizes above
+ * On success *out is a new context (free with gwas_destroy) and state_dev holds the replicated state.
+ * Synchronises; setup time is reported by gwas_timings (eig and precompute separately). */
+GWAS_API gwas_status gwas_setup(const gwas_options* opt, int64_t n, int64_t p, int64_t t,
+                       const double* phi, const double* XL, const double* Y,
+                       const double* h2, const double* sigma2,
+                       void* state_dev, size_t state_bytes, void* work_dev, size_t work_bytes,
+                       gwas_ctx** out);
+
+/* For ranks != 0 after state_dev was broadcast from a gwas_setup rank: validates the state header against
+ * (n, p, t, opt) and creates a context.  Synchronises. */
+GWAS_API gwas_status gwas_attach(const gwas_options* opt, int64_t n, int64_t p, int64_t t,
+                        void* state_dev, size_t state_bytes, void* work_dev, size_t work_bytes,
+                        gwas_ctx** out);
+
+/* Alg. 4 line 3 + lines 13-16 for ncols SNP columns.
+ *   XR     n x ncols, column-major with leading dimension ldx (elements, >= n), element type opt.xr_dtype.
+ *          Device pointer: ldx * sizeof(elem) must be a multiple of 16 and the address 16-byte aligned.
+ *          Host pointer: must be page-locked (cudaHostAlloc / cudaHostRegister); blocks of block_cols
+ *          columns are staged to HBM on copy_stream, double-buffered against compute (any ldx >= n).
+ *   b, var (device) ncols x t row-major ([i][j], trait fastest) in GWAS_OUT_SNP mode, or
+ *          ncols x t x w ([i][j][e], e = 0..p-1 the X_L coefficients, e = p the SNP) in GWAS_OUT_FULL mode;
+ *          var holds Var_gg (SNP mode) or the diagonal of Var (full mode).
+ *   status (device) ncols x t int8 (GWAS_PAIR_*).
+ * Asynchronous on compute_stream; XR and the outputs must stay valid until it completes. */
+GWAS_API gwas_status gwas_run(gwas_ctx* ctx, int64_t ncols, const void* XR, int64_t ldx,
+                     double* b, double* var, int8_t* status);
+
+/* Event-based times (ms): eigendecomposition, the rest of setup, and the sum of gwas_run calls' kernels
+ * (ms_run = K1 + K2 + K3 + H2D event sums; requires opt.timing).  Synchronises the compute stream. */
+GWAS_API gwas_status gwas_timings(gwas_ctx* ctx, double* ms_eig, double* ms_precompute, double* ms_run);
+
+/* Per-kernel event sums since the last reset (requires opt.timing): ms[GWAS_K1..GWAS_H2D] and launch counts.
+ * reset != 0 clears them after reading.  Synchronises the compute and copy streams. */
+GWAS_API gwas_status gwas_kernel_times(gwas_ctx* ctx, double* ms, int64_t* launches, int32_t reset);
+
+/* Unit-test entry to the K1/K2 kernel itself (no context):  C[i][c] = sum_r A(r, i) * B(r, c) for
+ * i < M, c < N, r < K, with A column-major K x M (ld lda; uint8 if a_u8 else fp64) and B column-major K x N
+ * (ld ldb), C row-major M x N (ld ldc); columns c >= nsq use A(r,i)^2 (K2's squared block; pass
+ * nsq >= N for a plain product).  All device pointers; lda*elem and ldb*8 multiples of 16, ldc even. */
+GWAS_API gwas_status gwas_gemm_tn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int32_t a_u8,
+                         const double* B, int64_t ldb, double* C, int64_t ldc, int64_t nsq, void* stream);
+
+GWAS_API void gwas_destroy(gwas_ctx* ctx);      /* frees the context only, nothing caller-owned */
+GWAS_API const char* gwas_last_error(void);     /* thread-local message of the last failing call ("" if none) */
+GWAS_API const char* gwas_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GWAS_H */

@@ -1,0 +1,253 @@
+// K1 / K2: FP64 tensor-core (DMMA) GEMM for sm_100a, C[M x N] = A[M x K] * B[N x K]^T (both K-contiguous).
+//
+//   K1 (Alg. 4 line 3, "X_R := Z^T X_R"):  A = X_R block (u8 dosages or fp64, one SNP per
+//       row of A), B = Z (column k of dsyevd's Z = row k of B), C = X_R'^T (one rotated SNP per row of C).
+//   K2 (Alg. 4 lines 13-15, all traits at once):  A = X_R'^T, B = [B_op | D] where
+//       B_op[:, f*t+j] = d_j * X_L'[:, f] (f < p), B_op[:, p*t+j] = d_j * y'_j, D[:, j] = d_j; columns >= nsq
+//       use A∘A, so C[i, nsq + j] = sum_k X_R'[k,i]^2 d_j[k] = W_R^T W_R (the K of K K^T = D never appears).
+//
+// Design: FP64 has no tcgen05 kind on sm_100a -- every .f64 mma lowers to
+// DMMA.8x8x4 (F2), issued per warp.  Operands are staged by TMA (cp.async.bulk.tensor, 128-byte swizzle for
+// fp64 tiles, OOB zero fill for the K / M / N tails) into a STAGES-deep ring guarded by mbarriers; one
+// thread issues TMA two tiles behind the slowest consumer, 8 warps each own a 64 x 32 accumulator tile
+// (64 doubles / thread) and run m8n8k4 DMMA from swizzled shared memory (conflict-free 64-bit fragment loads).  u8 dosages are
+// expanded to fp64 through a 256-entry shared-memory table (exact; no FP64-pipe conversion work).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gw {
+
+constexpr int GEMM_BK = 16;                 // K elements per stage (one 128-byte fp64 row)
+constexpr int GEMM_CONSUMER_WARPS = 8;
+constexpr int GEMM_THREADS = GEMM_CONSUMER_WARPS * 32;
+
+struct GemmShape {
+  int M, N, K;
+  double* C;
+  long long ldc;
+  int nsq;        // first column using A∘A (>= N: none)
+  int tiles_m, tiles_n;
+  int group_m;    // rasterisation group along M (L2 reuse of B panels)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Spin until the phase with the given parity has completed.  A bounded spin traps instead of hanging the
+// GPU if a pipeline bug ever loses an arrival (the trap surfaces as a launch failure on the host).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  long long spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (++spins > (1ll << 32)) __trap();
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Byte offset of fp64 element (row r, k) inside a [rows][16] fp64 tile written by TMA with SWIZZLE_128B
+// (16-byte chunk index XOR (row & 7); tile base 1024-byte aligned).
+__device__ __forceinline__ uint32_t swz128_off(int r, int k) {
+  return (uint32_t)(r * 128 + ((((k >> 1) ^ (r & 7)) & 7) << 4) + ((k & 1) << 3));
+}
+
+template <typename TA>
+struct ATile;
+template <>
+struct ATile<uint8_t> {
+  static constexpr int kBytesPerRow = GEMM_BK;  // 16 dosages, no swizzle (conflict-free: 4 lanes share a word)
+};
+template <>
+struct ATile<double> {
+  static constexpr int kBytesPerRow = GEMM_BK * 8;
+};
+
+template <typename TA, int BM, int BN>
+struct GemmSmem {
+  static constexpr int kATile = BM * ATile<TA>::kBytesPerRow;
+  static constexpr int kBTile = BN * GEMM_BK * 8;
+  static constexpr int kAStride = (kATile + 1023) / 1024 * 1024;
+  static constexpr int kBStride = (kBTile + 1023) / 1024 * 1024;
+};
+
+template <typename TA>
+__device__ __forceinline__ double load_a(const uint8_t* a_tile, const double* lut, int r, int k);
+
+template <>
+__device__ __forceinline__ double load_a<uint8_t>(const uint8_t* a_tile, const double* lut, int r, int k) {
+  return lut[a_tile[r * GEMM_BK + k]];
+}
+template <>
+__device__ __forceinline__ double load_a<double>(const uint8_t* a_tile, const double* lut, int r, int k) {
+  return *reinterpret_cast<const double*>(a_tile + swz128_off(r, k));
+}
+
+// One CTA computes a BM x BN tile of C with 8 warps (warp grid 2 x 4 for 128 x 128); thread 0 also issues TMA.
+template <typename TA, int BM, int BN, int STAGES, bool SQ>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tn_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape s) {
+  constexpr int WARPS_N = 4;
+  constexpr int WARPS_M = GEMM_CONSUMER_WARPS / WARPS_N;
+  constexpr int WM = BM / WARPS_M;  // 64
+  constexpr int WN = BN / WARPS_N;  // 32
+  constexpr int MI = WM / 8, NI = WN / 8;
+  using L = GemmSmem<TA, BM, BN>;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;
+  uint8_t* sA = sB + STAGES * L::kBStride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + STAGES * L::kAStride);
+  uint64_t* empty = full + STAGES;
+  double* lut = reinterpret_cast<double*>(empty + STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // grouped rasterisation: consecutive CTAs walk down a group of group_m row tiles, then move along N
+  int tm, tn;
+  {
+    const int pid = blockIdx.x;
+    const int per_group = s.group_m * s.tiles_n;
+    const int g = pid / per_group;
+    const int first_m = g * s.group_m;
+    const int gsz = min(s.tiles_m - first_m, s.group_m);
+    const int r = pid - g * per_group;
+    tm = first_m + r % gsz;
+    tn = r / gsz;
+  }
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int KT = (s.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], GEMM_CONSUMER_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (sizeof(TA) == 1) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = (double)i;
+  }
+  __syncthreads();
+
+  // Producer = thread 0 (also a consumer lane): tiles 0..STAGES-2 up front, then in iteration kt it refills
+  // tile kt+STAGES-2 into the slot freed by tile kt-2 (two iterations of slack, so the empty-barrier wait
+  // almost never blocks).  No dedicated producer warp: 8 warps keep 255 registers/thread available.
+  auto produce = [&](int kf) {
+    const int st = kf % STAGES;
+    if (kf >= STAGES) mbar_wait(&empty[st], ((kf / STAGES) - 1) & 1);
+    mbar_expect_tx(&full[st], L::kATile + L::kBTile);
+    tma_load_2d(sA + st * L::kAStride, &tmA, &full[st], kf * GEMM_BK, m0);
+    tma_load_2d(sB + st * L::kBStride, &tmB, &full[st], kf * GEMM_BK, n0);
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int kf = 0; kf < STAGES - 1 && kf < KT; ++kf) produce(kf);
+  }
+
+  // ---------------- consumers
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[MI][NI][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // K2: which of this warp's 8-column fragments take the squared A operand (nsq is a multiple of 8)
+  bool sq[NI];
+  bool any_sq = false;
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    sq[j] = SQ && (n0 + wn * WN + j * 8 >= s.nsq);
+    any_sq |= sq[j];
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % STAGES;
+    if (threadIdx.x == 0 && kt >= 1 && kt + STAGES - 2 < KT) produce(kt + STAGES - 2);
+    __syncwarp();
+    mbar_wait(&full[st], (kt / STAGES) & 1);
+    const uint8_t* a_tile = sA + st * L::kAStride;
+    const uint8_t* b_tile = sB + st * L::kBStride;
+#pragma unroll
+    for (int ks = 0; ks < GEMM_BK / 4; ++ks) {
+      const int k = ks * 4 + q;
+      double a[MI], b[NI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = load_a<TA>(a_tile, lut, wm * WM + i * 8 + g, k);
+#pragma unroll
+      for (int j = 0; j < NI; ++j) b[j] = *reinterpret_cast<const double*>(b_tile + swz128_off(wn * WN + j * 8 + g, k));
+      if (SQ && any_sq) {
+        double a2[MI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a2[i] = a[i] * a[i];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j], sq[j] ? a2[i] : a[i], b[j]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+  // ---------------- epilogue: each lane owns C[row][2q, 2q+1] of every 8x8 fragment
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int row = m0 + wm * WM + i * 8 + g;
+    if (row >= s.M) continue;
+    double* crow = s.C + (long long)row * s.ldc;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const int col = n0 + wn * WN + j * 8 + 2 * q;
+      if (col + 1 < s.N) {
+        *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else if (col < s.N) {
+        crow[col] = acc[i][j][0];
+      }
+    }
+  }
+}
+
+}  // namespace gw

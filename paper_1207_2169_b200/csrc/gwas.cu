@@ -1,0 +1,733 @@
+// libgwas.so -- C-ABI and runtime of the B200-native CLAK-Eig GLS-sequence hot path.
+// See include/gwas.h for the contract and DESIGN.md for the design; the kernels live in gemm_dmma.cuh (K1/K2),
+// schur.cuh (K3) and setup_kernels.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gwas.h"
+#include "gemm_dmma.cuh"
+#include "schur.cuh"
+#include "setup_kernels.cuh"
+
+namespace {
+
+constexpr uint64_t kMagic = 0x4b414c4353415747ull;  // "GWASCLAK"
+constexpr int64_t kVersion = 1;
+constexpr int kPMax = 12;
+
+thread_local std::string g_err;
+
+gwas_status fail(gwas_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CKC(x)                                                                                  \
+  do {                                                                                          \
+    cudaError_t e__ = (x);                                                                      \
+    if (e__ != cudaSuccess) return fail(GWAS_E_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e__), \
+                                        __FILE__, __LINE__);                                    \
+  } while (0)
+
+#define CKS(x)                                                                                     \
+  do {                                                                                             \
+    cusolverStatus_t s__ = (x);                                                                    \
+    if (s__ != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "%s: cusolver status %d", #x, (int)s__); \
+  } while (0)
+
+#define CKG(x)                              \
+  do {                                      \
+    gwas_status g__ = (x);                  \
+    if (g__ != GWAS_OK) return g__;         \
+  } while (0)
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline size_t align256(size_t a) { return (a + 255) / 256 * 256; }
+
+struct StateHeader {
+  uint64_t magic;
+  int64_t version;
+  int64_t n, p, t, kpad, nsq, n2;
+  int32_t output_mode, var_convention;
+  double eps_collinear;
+  int64_t off_Z, off_W, off_B2, off_Lpk, off_v, off_s2, off_betaT, off_dinv, total;
+};
+constexpr size_t kHeaderBytes = 512;
+static_assert(sizeof(StateHeader) <= kHeaderBytes, "header");
+
+struct Dims {
+  int64_t n, p, t, kpad, nsq, n2, ldc2, lds, kb;
+  size_t es;
+};
+
+Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
+  Dims d;
+  d.n = n;
+  d.p = p;
+  d.t = t;
+  d.kpad = round_up(n, 16);
+  d.nsq = round_up(t * (p + 1), 8);
+  d.n2 = d.nsq + t;
+  d.ldc2 = round_up(d.n2, 2);
+  d.lds = round_up(t * (p + 1), 2);
+  d.kb = o->block_cols > 0 ? o->block_cols : 8192;
+  d.es = o->xr_dtype == GWAS_XR_U8 ? 1 : 8;
+  return d;
+}
+
+StateHeader make_header(const Dims& d, const gwas_options* o) {
+  StateHeader h;
+  memset(&h, 0, sizeof(h));
+  h.magic = kMagic;
+  h.version = kVersion;
+  h.n = d.n;
+  h.p = d.p;
+  h.t = d.t;
+  h.kpad = d.kpad;
+  h.nsq = d.nsq;
+  h.n2 = d.n2;
+  h.output_mode = o->output_mode;
+  h.var_convention = o->var_convention;
+  h.eps_collinear = o->eps_collinear;
+  size_t off = kHeaderBytes;
+  auto take = [&](size_t bytes) {
+    size_t r = off;
+    off = align256(off + bytes);
+    return (int64_t)r;
+  };
+  h.off_Z = take(sizeof(double) * d.kpad * d.kpad);
+  h.off_W = take(sizeof(double) * d.kpad);
+  h.off_B2 = take(sizeof(double) * d.n2 * d.kpad);
+  const int64_t npk = d.p * (d.p + 1) / 2;
+  h.off_Lpk = take(sizeof(double) * npk * d.t);
+  h.off_v = take(sizeof(double) * d.p * d.t);
+  h.off_s2 = take(sizeof(double) * d.t);
+  h.off_betaT = take(sizeof(double) * d.p * d.t);
+  h.off_dinv = take(sizeof(double) * d.p * d.t);
+  h.total = (int64_t)off;
+  return h;
+}
+
+struct RunLayout {
+  size_t stage[2], xrp, c2, total;
+};
+RunLayout run_layout(const Dims& d) {
+  RunLayout r;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t x = off;
+    off = align256(off + bytes);
+    return x;
+  };
+  r.stage[0] = take(d.es * d.kpad * d.kb);
+  r.stage[1] = take(d.es * d.kpad * d.kb);
+  r.xrp = take(sizeof(double) * d.kpad * d.kb);
+  r.c2 = take(sizeof(double) * d.ldc2 * d.kb);
+  r.total = off;
+  return r;
+}
+
+struct SetupLayout {
+  size_t xlpad, ypad, xlp, yp, stl, h2, s2, err, info, work, total;
+};
+SetupLayout setup_layout(const Dims& d, int64_t lwork) {
+  SetupLayout s;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t x = off;
+    off = align256(off + bytes);
+    return x;
+  };
+  s.xlpad = take(sizeof(double) * d.p * d.kpad);
+  s.ypad = take(sizeof(double) * d.t * d.kpad);
+  s.xlp = take(sizeof(double) * d.p * d.kpad);
+  s.yp = take(sizeof(double) * d.t * d.kpad);
+  s.stl = take(sizeof(double) * d.p * d.lds);
+  s.h2 = take(sizeof(double) * d.t);
+  s.s2 = take(sizeof(double) * d.t);
+  s.err = take(sizeof(unsigned long long) * 4);
+  s.info = take(sizeof(int) * 4);
+  s.work = take(sizeof(double) * (size_t)std::max<int64_t>(lwork, 1));
+  s.total = off;
+  return s;
+}
+
+gwas_status check_sizes(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
+  if (!o) return fail(GWAS_E_ARG, "options is NULL");
+  if (p < 1 || p > kPMax) return fail(GWAS_E_ARG, "p = %lld outside [1, %d]", (long long)p, kPMax);
+  if (t < 1) return fail(GWAS_E_ARG, "t = %lld < 1", (long long)t);
+  if (n < p + 1) return fail(GWAS_E_ARG, "n = %lld < p + 1 = %lld", (long long)n, (long long)p + 1);
+  if (n > (1ll << 31) / 16) return fail(GWAS_E_ARG, "n = %lld too large", (long long)n);
+  if (o->xr_dtype != GWAS_XR_F64 && o->xr_dtype != GWAS_XR_U8) return fail(GWAS_E_ARG, "bad xr_dtype");
+  if (o->output_mode != GWAS_OUT_SNP && o->output_mode != GWAS_OUT_FULL) return fail(GWAS_E_ARG, "bad output_mode");
+  if (o->var_convention != GWAS_VAR_TEXTBOOK && o->var_convention != GWAS_VAR_LITERAL)
+    return fail(GWAS_E_ARG, "bad var_convention");
+  if (o->block_cols < 0 || o->block_cols > (1ll << 22)) return fail(GWAS_E_ARG, "bad block_cols");
+  if (!(o->eps_spd >= 0) || !(o->eps_collinear >= 0)) return fail(GWAS_E_ARG, "bad eps");
+  const int64_t t_p2 = t * (p + 2) + 8;
+  if (t_p2 > (1ll << 31) - 1) return fail(GWAS_E_ARG, "t too large");
+  return GWAS_OK;
+}
+
+gwas_status dsyevd_lwork(int device, int64_t n, int64_t kpad, int64_t* lwork) {
+  CKC(cudaSetDevice(device));
+  cusolverDnHandle_t h;
+  CKS(cusolverDnCreate(&h));
+  int lw = 0;
+  cusolverStatus_t s = cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n,
+                                                   nullptr, (int)kpad, nullptr, &lw);
+  cusolverDnDestroy(h);
+  if (s != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "dsyevd_bufferSize status %d", (int)s);
+  *lwork = lw;
+  return GWAS_OK;
+}
+
+// ------------------------------------------------------------------ TMA descriptors + GEMM launch
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+gwas_status get_encoder() {
+  if (g_encode) return GWAS_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CKC(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !fn) return fail(GWAS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return GWAS_OK;
+}
+
+// 2-D K-contiguous operand: rows x K elements, leading dimension ld (elements); box = 16 x box_rows.
+gwas_status make_map(CUtensorMap* map, const void* ptr, bool u8, int64_t K, int64_t rows, int64_t ld, int box_rows) {
+  CKG(get_encoder());
+  const size_t es = u8 ? 1 : 8;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)gw::GEMM_BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * es) & 15))
+    return fail(GWAS_E_ARG, "operand not 16-byte aligned (ptr %p, ld %lld)", ptr, (long long)ld);
+  CUresult r = g_encode(map, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        u8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(GWAS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return GWAS_OK;
+}
+
+constexpr int kBM = 128, kBN = 128;
+constexpr int kStagesU8 = 8, kStagesF64 = 6;
+
+template <typename TA, int STAGES>
+constexpr size_t gemm_smem_bytes() {
+  using L = gw::GemmSmem<TA, kBM, kBN>;
+  return 1024 + STAGES * (L::kAStride + L::kBStride) + 2 * STAGES * sizeof(uint64_t) + 256 * sizeof(double);
+}
+
+template <typename TA, int STAGES, bool SQ>
+gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw::GemmShape& s, cudaStream_t st) {
+  static bool attr_set = false;  // per instantiation (the library binds one device per process)
+  constexpr size_t smem = gemm_smem_bytes<TA, STAGES>();
+  auto kern = gw::gemm_tn_dmma<TA, kBM, kBN, STAGES, SQ>;
+  if (!attr_set) {
+    CKC(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const int grid = s.tiles_m * s.tiles_n;
+  kern<<<grid, gw::GEMM_THREADS, smem, st>>>(ma, mb, s);
+  CKC(cudaGetLastError());
+  return GWAS_OK;
+}
+
+// C[M x N] (row-major, ldc) = A[M x K] (rows K-contiguous, lda) * B[N x K]^T (rows K-contiguous, ldb)
+gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                    int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return GWAS_OK;
+  if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
+  if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return fail(GWAS_E_ARG, "gemm dims too large");
+  CUtensorMap ma, mb;
+  CKG(make_map(&ma, A, a_u8, K, M, lda, kBM));
+  CKG(make_map(&mb, B, false, K, N, ldb, kBN));
+  gw::GemmShape s;
+  s.M = (int)M;
+  s.N = (int)N;
+  s.K = (int)K;
+  s.C = C;
+  s.ldc = ldc;
+  s.nsq = (int)std::min<int64_t>(nsq, N);
+  s.tiles_m = (int)((M + kBM - 1) / kBM);
+  s.tiles_n = (int)((N + kBN - 1) / kBN);
+  s.group_m = 16;
+  const bool sq = nsq < N;
+  if (sq && (nsq % 8)) return fail(GWAS_E_ARG, "nsq must be a multiple of 8");
+  if (a_u8) {
+    if (sq) return launch_gemm_t<uint8_t, kStagesU8, true>(ma, mb, s, st);
+    return launch_gemm_t<uint8_t, kStagesU8, false>(ma, mb, s, st);
+  }
+  if (sq) return launch_gemm_t<double, kStagesF64, true>(ma, mb, s, st);
+  return launch_gemm_t<double, kStagesF64, false>(ma, mb, s, st);
+}
+
+gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
+  const long long np = (long long)a.cols * a.t;
+  if (np == 0) return GWAS_OK;
+  const int threads = 256;
+  const unsigned grid = (unsigned)((np + threads - 1) / threads);
+  switch (p) {
+#define CASE_P(P) \
+  case P: gw::schur_solve<P><<<grid, threads, 0, st>>>(a); break;
+    CASE_P(1) CASE_P(2) CASE_P(3) CASE_P(4) CASE_P(5) CASE_P(6)
+    CASE_P(7) CASE_P(8) CASE_P(9) CASE_P(10) CASE_P(11) CASE_P(12)
+#undef CASE_P
+    default:
+      return fail(GWAS_E_ARG, "p = %d unsupported", p);
+  }
+  CKC(cudaGetLastError());
+  return GWAS_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct gwas_ctx {
+  gwas_options opt;
+  Dims d;
+  StateHeader h;
+  uint8_t* state = nullptr;
+  uint8_t* work = nullptr;
+  size_t work_bytes = 0;
+  RunLayout rl;
+  cudaStream_t cs = nullptr, ps = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  int stage_next = 0;
+  bool stage_zeroed = false;
+  float ms_eig = 0.f, ms_pre = 0.f;
+  // per-kernel event timers
+  struct Pending {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms_acc[GWAS_NUM_TIMERS] = {0, 0, 0, 0};
+  int64_t launches[GWAS_NUM_TIMERS] = {0, 0, 0, 0};
+
+  double* Z() const { return reinterpret_cast<double*>(state + h.off_Z); }
+  double* W() const { return reinterpret_cast<double*>(state + h.off_W); }
+  double* B2() const { return reinterpret_cast<double*>(state + h.off_B2); }
+  double* Lpk() const { return reinterpret_cast<double*>(state + h.off_Lpk); }
+  double* v() const { return reinterpret_cast<double*>(state + h.off_v); }
+  double* s2() const { return reinterpret_cast<double*>(state + h.off_s2); }
+  double* betaT() const { return reinterpret_cast<double*>(state + h.off_betaT); }
+  double* dinv() const { return reinterpret_cast<double*>(state + h.off_dinv); }
+
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  gwas_status tic(int kind, cudaStream_t st, cudaEvent_t* out) {
+    *out = nullptr;
+    if (!opt.timing) return GWAS_OK;
+    *out = ev();
+    CKC(cudaEventRecord(*out, st));
+    pending.push_back({kind, *out, nullptr});
+    return GWAS_OK;
+  }
+  gwas_status toc(cudaStream_t st) {
+    if (!opt.timing) return GWAS_OK;
+    cudaEvent_t e = ev();
+    CKC(cudaEventRecord(e, st));
+    pending.back().b = e;
+    return GWAS_OK;
+  }
+  gwas_status drain() {
+    for (auto& pd : pending) {
+      CKC(cudaEventSynchronize(pd.b));
+      float ms = 0.f;
+      CKC(cudaEventElapsedTime(&ms, pd.a, pd.b));
+      ms_acc[pd.kind] += ms;
+      launches[pd.kind] += 1;
+      pool.push_back(pd.a);
+      pool.push_back(pd.b);
+    }
+    pending.clear();
+    return GWAS_OK;
+  }
+};
+
+namespace {
+
+gwas_status ctx_init(gwas_ctx* c, const gwas_options* o, const Dims& d, const StateHeader& h, void* state,
+                     void* work, size_t work_bytes) {
+  c->opt = *o;
+  c->d = d;
+  c->h = h;
+  c->state = static_cast<uint8_t*>(state);
+  c->work = static_cast<uint8_t*>(work);
+  c->work_bytes = work_bytes;
+  c->rl = run_layout(d);
+  c->cs = static_cast<cudaStream_t>(o->compute_stream);
+  c->ps = o->copy_stream ? static_cast<cudaStream_t>(o->copy_stream) : c->cs;
+  for (int i = 0; i < 2; ++i) {
+    CKC(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
+  }
+  return GWAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void gwas_default_options(gwas_options* o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->device = 0;
+  o->xr_dtype = GWAS_XR_U8;
+  o->output_mode = GWAS_OUT_SNP;
+  o->var_convention = GWAS_VAR_TEXTBOOK;
+  o->block_cols = 8192;
+  o->eps_spd = 1e-10;
+  o->eps_collinear = 1e-10;
+  o->compute_stream = nullptr;
+  o->copy_stream = nullptr;
+  o->timing = 0;
+}
+
+const char* gwas_last_error(void) { return g_err.c_str(); }
+const char* gwas_version(void) { return "gwas-clak-eig-b200 1 (sm_100a, FP64 DMMA)"; }
+
+size_t gwas_state_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
+  if (check_sizes(n, p, t, o) != GWAS_OK) return 0;
+  Dims d = make_dims(n, p, t, o);
+  return (size_t)make_header(d, o).total;
+}
+
+size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
+  if (check_sizes(n, p, t, o) != GWAS_OK) return 0;
+  Dims d = make_dims(n, p, t, o);
+  int64_t lwork = 0;
+  if (dsyevd_lwork(o->device, n, d.kpad, &lwork) != GWAS_OK) return 0;
+  return std::max(setup_layout(d, lwork).total, run_layout(d).total);
+}
+
+gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, const double* phi, const double* XL,
+                       const double* Y, const double* h2, const double* sigma2, void* state_dev, size_t state_bytes,
+                       void* work_dev, size_t work_bytes, gwas_ctx** out) {
+  g_err.clear();
+  CKG(check_sizes(n, p, t, o));
+  if (!out || !phi || !XL || !Y || !h2 || !sigma2 || !state_dev || !work_dev)
+    return fail(GWAS_E_ARG, "NULL pointer argument");
+  *out = nullptr;
+  CKC(cudaSetDevice(o->device));
+  Dims d = make_dims(n, p, t, o);
+  StateHeader h = make_header(d, o);
+  int64_t lwork = 0;
+  CKG(dsyevd_lwork(o->device, n, d.kpad, &lwork));
+  SetupLayout sl = setup_layout(d, lwork);
+  RunLayout rl = run_layout(d);
+  if (state_bytes < (size_t)h.total) return fail(GWAS_E_NOMEM, "state %zu < %lld bytes", state_bytes, (long long)h.total);
+  if (work_bytes < std::max(sl.total, rl.total))
+    return fail(GWAS_E_NOMEM, "workspace %zu < %zu bytes", work_bytes, std::max(sl.total, rl.total));
+  if (!is_device_ptr(state_dev) || !is_device_ptr(work_dev)) return fail(GWAS_E_ARG, "state/work must be device memory");
+
+  // validate (h2, sigma2) on the host
+  std::vector<double> hh(t), ss(t);
+  CKC(cudaMemcpy(hh.data(), h2, sizeof(double) * t, cudaMemcpyDefault));
+  CKC(cudaMemcpy(ss.data(), sigma2, sizeof(double) * t, cudaMemcpyDefault));
+  for (int64_t j = 0; j < t; ++j) {
+    if (!(hh[j] >= 0.0 && hh[j] <= 1.0)) return fail(GWAS_E_ARG, "h2[%lld] = %g outside [0, 1]", (long long)j, hh[j]);
+    if (!(ss[j] > 0.0) || !std::isfinite(ss[j])) return fail(GWAS_E_ARG, "sigma2[%lld] = %g not > 0", (long long)j, ss[j]);
+  }
+
+  gwas_ctx* c = new gwas_ctx();
+  gwas_status st = ctx_init(c, o, d, h, state_dev, work_dev, work_bytes);
+  if (st != GWAS_OK) {
+    gwas_destroy(c);
+    return st;
+  }
+  cudaStream_t cs = c->cs;
+  uint8_t* w = c->work;
+  double* xlpad = reinterpret_cast<double*>(w + sl.xlpad);
+  double* ypad = reinterpret_cast<double*>(w + sl.ypad);
+  double* xlp = reinterpret_cast<double*>(w + sl.xlp);
+  double* yp = reinterpret_cast<double*>(w + sl.yp);
+  double* stl = reinterpret_cast<double*>(w + sl.stl);
+  double* dh2 = reinterpret_cast<double*>(w + sl.h2);
+  double* ds2 = reinterpret_cast<double*>(w + sl.s2);
+  unsigned long long* derr = reinterpret_cast<unsigned long long*>(w + sl.err);
+  int* dinfo = reinterpret_cast<int*>(w + sl.info);
+  double* dwork = reinterpret_cast<double*>(w + sl.work);
+
+  auto body = [&]() -> gwas_status {
+    cudaEvent_t e0, e1, e2, e3;
+    CKC(cudaEventCreate(&e0));
+    CKC(cudaEventCreate(&e1));
+    CKC(cudaEventCreate(&e2));
+    CKC(cudaEventCreate(&e3));
+    CKC(cudaEventRecord(e0, cs));
+    // header + Phi into Z (ld kpad, zero padding), W zero
+    CKC(cudaMemcpyAsync(c->state, &c->h, sizeof(StateHeader), cudaMemcpyHostToDevice, cs));
+    CKC(cudaMemsetAsync(c->Z(), 0, sizeof(double) * d.kpad * d.kpad, cs));
+    CKC(cudaMemsetAsync(c->W(), 0, sizeof(double) * d.kpad, cs));
+    CKC(cudaMemcpy2DAsync(c->Z(), sizeof(double) * d.kpad, phi, sizeof(double) * n, sizeof(double) * n, n,
+                          cudaMemcpyDefault, cs));
+    CKC(cudaMemcpyAsync(dh2, h2, sizeof(double) * t, cudaMemcpyDefault, cs));
+    CKC(cudaMemcpyAsync(ds2, sigma2, sizeof(double) * t, cudaMemcpyDefault, cs));
+    CKC(cudaMemcpyAsync(c->s2(), sigma2, sizeof(double) * t, cudaMemcpyDefault, cs));
+    CKC(cudaMemcpy2DAsync(xlpad, sizeof(double) * d.kpad, XL, sizeof(double) * n, sizeof(double) * n, p,
+                          cudaMemcpyDefault, cs));
+    CKC(cudaMemcpy2DAsync(ypad, sizeof(double) * d.kpad, Y, sizeof(double) * n, sizeof(double) * n, t,
+                          cudaMemcpyDefault, cs));
+    CKC(cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long) * 4, cs));
+    // Alg. 4 line 1: Phi = Z W Z^T, in place (Z overwrites Phi)
+    CKC(cudaEventRecord(e1, cs));
+    cusolverDnHandle_t hs;
+    CKS(cusolverDnCreate(&hs));
+    cusolverStatus_t ss2 = cusolverDnSetStream(hs, cs);
+    if (ss2 == CUSOLVER_STATUS_SUCCESS)
+      ss2 = cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, c->Z(), (int)d.kpad,
+                             c->W(), dwork, (int)lwork, dinfo);
+    CKC(cudaEventRecord(e2, cs));
+    CKC(cudaStreamSynchronize(cs));
+    cusolverDnDestroy(hs);
+    if (ss2 != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "cusolverDnDsyevd status %d", (int)ss2);
+    int info = 0;
+    CKC(cudaMemcpy(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+    if (info != 0) return fail(GWAS_E_EIG, "dsyevd info = %d", info);
+    // Alg. 4 lines 2, 4: X_L' = Z^T X_L, Y' = Z^T Y  (K1 kernel, fp64 A)
+    CKG(gemm_tn(false, xlpad, d.kpad, c->Z(), d.kpad, xlp, d.kpad, p, n, n, n, cs));
+    CKG(gemm_tn(false, ypad, d.kpad, c->Z(), d.kpad, yp, d.kpad, t, n, n, n, cs));
+    // Alg. 4 lines 6, 8, 9: D_j and the D_j-scaled operand B2 = [B_op | D]
+    {
+      dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)d.n2);
+      gw::build_b2<<<grid, 256, 0, cs>>>(xlp, yp, c->W(), dh2, ds2, (int)n, (int)p, (int)t, (int)d.kpad, (int)d.nsq,
+                                         (int)d.n2, o->eps_spd, c->B2(), derr);
+      CKC(cudaGetLastError());
+    }
+    // Alg. 4 lines 10-11: S_TL_j = X_L'^T D_j X_L', b_T_j = X_L'^T D_j y'_j for all j (K2 kernel)
+    CKG(gemm_tn(false, xlp, d.kpad, c->B2(), d.kpad, stl, d.lds, p, t * (p + 1), n, d.n2, cs));
+    gw::trait_factor<kPMax><<<(unsigned)((t + 127) / 128), 128, 0, cs>>>(stl, d.lds, (int)p, (int)t, c->Lpk(), c->v(),
+                                                                         c->betaT(), c->dinv(), derr + 1);
+    CKC(cudaGetLastError());
+    CKC(cudaEventRecord(e3, cs));
+    unsigned long long herr[2];
+    CKC(cudaMemcpyAsync(herr, derr, sizeof(herr), cudaMemcpyDeviceToHost, cs));
+    CKC(cudaStreamSynchronize(cs));
+    float ms_all = 0.f, ms_eig = 0.f;
+    CKC(cudaEventElapsedTime(&ms_all, e0, e3));
+    CKC(cudaEventElapsedTime(&ms_eig, e1, e2));
+    c->ms_eig = ms_eig;
+    c->ms_pre = ms_all - ms_eig;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+    if (herr[0] != ~0ull) {
+      const long long j = (long long)(herr[0] / (unsigned long long)n), k = (long long)(herr[0] % (unsigned long long)n);
+      double wk = 0.0;
+      CKC(cudaMemcpy(&wk, c->W() + k, sizeof(double), cudaMemcpyDeviceToHost));
+      return fail(GWAS_E_NOT_SPD, "trait %lld: sigma2 (h2 w_k + 1 - h2) <= eps_spd at eigen-index k = %lld (w_k = %g)",
+                  j, k, wk);
+    }
+    if (herr[1] != ~0ull)
+      return fail(GWAS_E_NOT_SPD, "trait %lld: S_TL = X_L'^T D_j X_L' not positive definite (X_L rank-deficient?)",
+                  (long long)herr[1]);
+    return GWAS_OK;
+  };
+  st = body();
+  if (st != GWAS_OK) {
+    gwas_destroy(c);
+    return st;
+  }
+  *out = c;
+  return GWAS_OK;
+}
+
+gwas_status gwas_attach(const gwas_options* o, int64_t n, int64_t p, int64_t t, void* state_dev, size_t state_bytes,
+                        void* work_dev, size_t work_bytes, gwas_ctx** out) {
+  g_err.clear();
+  CKG(check_sizes(n, p, t, o));
+  if (!out || !state_dev || !work_dev) return fail(GWAS_E_ARG, "NULL pointer argument");
+  *out = nullptr;
+  CKC(cudaSetDevice(o->device));
+  Dims d = make_dims(n, p, t, o);
+  StateHeader want = make_header(d, o);
+  if (state_bytes < (size_t)want.total) return fail(GWAS_E_NOMEM, "state buffer too small");
+  RunLayout rl = run_layout(d);
+  if (work_bytes < rl.total) return fail(GWAS_E_NOMEM, "workspace %zu < %zu bytes", work_bytes, rl.total);
+  StateHeader got;
+  CKC(cudaMemcpy(&got, state_dev, sizeof(got), cudaMemcpyDeviceToHost));
+  if (got.magic != kMagic || got.version != kVersion || got.n != n || got.p != p || got.t != t ||
+      got.total != want.total || got.output_mode != o->output_mode || got.var_convention != o->var_convention)
+    return fail(GWAS_E_STATE, "state header does not match (n, p, t, options)");
+  gwas_ctx* c = new gwas_ctx();
+  gwas_status st = ctx_init(c, o, d, got, state_dev, work_dev, work_bytes);
+  if (st != GWAS_OK) {
+    gwas_destroy(c);
+    return st;
+  }
+  *out = c;
+  return GWAS_OK;
+}
+
+gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, double* b, double* var, int8_t* status) {
+  g_err.clear();
+  if (!c) return fail(GWAS_E_STATE, "NULL context");
+  if (ncols < 0) return fail(GWAS_E_ARG, "ncols < 0");
+  if (ncols == 0) return GWAS_OK;
+  if (!XR || !b || !var || !status) return fail(GWAS_E_ARG, "NULL pointer argument");
+  const Dims& d = c->d;
+  if (ldx < d.n) return fail(GWAS_E_ARG, "ldx = %lld < n = %lld", (long long)ldx, (long long)d.n);
+  CKC(cudaSetDevice(c->opt.device));
+  const bool dev = is_device_ptr(XR);
+  if (!dev && !is_pinned_host(XR)) return fail(GWAS_E_ARG, "X_R host buffer is not page-locked (use pinned memory)");
+  if (dev && (((ldx * (int64_t)d.es) & 15) || (reinterpret_cast<uintptr_t>(XR) & 15)))
+    return fail(GWAS_E_ARG, "device X_R: ldx * elem_size must be a multiple of 16 and XR 16-byte aligned");
+  const bool u8 = c->opt.xr_dtype == GWAS_XR_U8;
+  const int64_t w = d.p + 1;
+  const int64_t per_pair = c->opt.output_mode == GWAS_OUT_FULL ? w : 1;
+  cudaStream_t cs = c->cs, ps = c->ps;
+  double* xrp = reinterpret_cast<double*>(c->work + c->rl.xrp);
+  double* c2 = reinterpret_cast<double*>(c->work + c->rl.c2);
+  cudaEvent_t dummy;
+  for (int64_t blk = 0; blk < ncols; blk += d.kb) {
+    const int64_t cols = std::min<int64_t>(d.kb, ncols - blk);
+    const uint8_t* src = static_cast<const uint8_t*>(XR) + blk * ldx * (int64_t)d.es;
+    const void* A = src;
+    int64_t lda = ldx;
+    int s = -1;
+    if (!dev) {
+      // H1 staging (P:158, P:210 double buffering -> host->HBM on the copy stream)
+      s = c->stage_next;
+      c->stage_next ^= 1;
+      void* stage = c->work + c->rl.stage[s];
+      CKC(cudaStreamWaitEvent(ps, c->ev_free[s], 0));
+      CKG(c->tic(GWAS_H2D, ps, &dummy));
+      if (ldx == d.kpad) {
+        CKC(cudaMemcpyAsync(stage, src, (size_t)((cols - 1) * ldx + d.n) * d.es, cudaMemcpyHostToDevice, ps));
+      } else {
+        CKC(cudaMemcpy2DAsync(stage, (size_t)d.kpad * d.es, src, (size_t)ldx * d.es, (size_t)d.n * d.es, (size_t)cols,
+                              cudaMemcpyHostToDevice, ps));
+      }
+      CKG(c->toc(ps));
+      CKC(cudaEventRecord(c->ev_in[s], ps));
+      CKC(cudaStreamWaitEvent(cs, c->ev_in[s], 0));
+      A = stage;
+      lda = d.kpad;
+    }
+    // K1 (Alg. 4 line 3): X_R'^T = X_R^T Z  (row i of xrp = Z^T g_i)
+    CKG(c->tic(GWAS_K1, cs, &dummy));
+    CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs));
+    CKG(c->toc(cs));
+    if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
+    // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
+    CKG(c->tic(GWAS_K2, cs, &dummy));
+    CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs));
+    CKG(c->toc(cs));
+    // K3 (Alg. 4 line 16): b_ij := S^-1 b_ij by Schur complement
+    gw::SchurArgs a;
+    a.C = c2;
+    a.ldc = d.ldc2;
+    a.nsq = (int)d.nsq;
+    a.cols = (int)cols;
+    a.t = (int)d.t;
+    a.Lpk = c->Lpk();
+    a.v = c->v();
+    a.s2 = c->s2();
+    a.betaT = c->betaT();
+    a.dinv = c->dinv();
+    a.eps_collinear = c->opt.eps_collinear;
+    a.literal = c->opt.var_convention == GWAS_VAR_LITERAL;
+    a.full = c->opt.output_mode == GWAS_OUT_FULL;
+    a.b = b + blk * d.t * per_pair;
+    a.var = var + blk * d.t * per_pair;
+    a.status = status + blk * d.t;
+    CKG(c->tic(GWAS_K3, cs, &dummy));
+    CKG(launch_schur(a, (int)d.p, cs));
+    CKG(c->toc(cs));
+  }
+  return GWAS_OK;
+}
+
+gwas_status gwas_timings(gwas_ctx* c, double* ms_eig, double* ms_pre, double* ms_run) {
+  if (!c) return fail(GWAS_E_STATE, "NULL context");
+  CKG(c->drain());
+  if (ms_eig) *ms_eig = c->ms_eig;
+  if (ms_pre) *ms_pre = c->ms_pre;
+  if (ms_run) *ms_run = c->ms_acc[0] + c->ms_acc[1] + c->ms_acc[2] + c->ms_acc[3];
+  return GWAS_OK;
+}
+
+gwas_status gwas_kernel_times(gwas_ctx* c, double* ms, int64_t* launches, int32_t reset) {
+  if (!c) return fail(GWAS_E_STATE, "NULL context");
+  CKG(c->drain());
+  for (int k = 0; k < GWAS_NUM_TIMERS; ++k) {
+    if (ms) ms[k] = c->ms_acc[k];
+    if (launches) launches[k] = c->launches[k];
+    if (reset) {
+      c->ms_acc[k] = 0;
+      c->launches[k] = 0;
+    }
+  }
+  return GWAS_OK;
+}
+
+gwas_status gwas_gemm_tn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int32_t a_u8, const double* B,
+                         int64_t ldb, double* C, int64_t ldc, int64_t nsq, void* stream) {
+  g_err.clear();
+  if (!A || !B || !C) return fail(GWAS_E_ARG, "NULL pointer argument");
+  if (lda < K || ldb < K || ldc < N) return fail(GWAS_E_ARG, "leading dimension too small");
+  return gemm_tn(a_u8 != 0, A, lda, B, ldb, C, ldc, M, N, K, nsq, static_cast<cudaStream_t>(stream));
+}
+
+void gwas_destroy(gwas_ctx* c) {
+  if (!c) return;
+  c->drain();
+  for (auto e : c->pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+    if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+  }
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// K3: batched bordered solve by Schur complement (Alg. 4 lines 14-16).
+//
+// For pair (i, j) the normal equations of X_i = [X_L | g_i] in the M_j^-1 inner product are the bordered
+// system
+//        [ S_TL_j   a_ij ] [b_L]   [ b_T_j ]        a_ij = X_L'^T D_j x_i'     (p values, C[i, f t + j])
+//        [ a_ij^T   c_ij ] [b_g] = [ r_ij  ]        c_ij = x_i'^T D_j x_i'     (C[i, nsq + j])
+//                                                   r_ij = x_i'^T D_j y_j'     (C[i, p t + j])
+// With S_TL_j = L_j L_j^T and v_j = L_j^-1 b_T_j precomputed in setup:
+//        u = L_j^-1 a,  sigma = c - u.u  (Schur complement = last squared Cholesky pivot of S),
+//        b_g = (r - u.v_j) / sigma,  Var_gg = 1 / sigma                        (textbook Var, reading A1)
+//   full output mode adds q = L_j^-T u,  b_L = S_TL_j^-1 b_T_j - q b_g,  diag Var_L = diag(S_TL_j^-1) + q^2/sigma.
+// Collinear SNP (reading A6): sigma <= eps * c -> status 1, NaN payload; non-finite -> status 2.
+// One thread per pair, trait index fastest, so a warp reads 32 consecutive traits of one C row (coalesced)
+// and writes 32 consecutive outputs.  HBM-bound: 8(p+2) bytes in, 17 (SNP mode) bytes out per pair.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gw {
+
+struct SchurArgs {
+  const double* C;    // cols x ldc (row i = SNP i of the block)
+  long long ldc;
+  int nsq;            // column offset of the c_ij block
+  int cols, t;
+  const double* Lpk;  // [e][j], e = f(f+1)/2 + l (packed lower L_TL_j, row-major)
+  const double* v;    // [f][j]
+  const double* s2;   // [j]
+  const double* betaT;  // [f][j] = S_TL_j^-1 b_T_j  (full mode)
+  const double* dinv;   // [f][j] = diag(S_TL_j^-1) (full mode)
+  double eps_collinear;
+  int literal;        // var_convention 1: Var *= sigma2_j
+  int full;           // output mode
+  double* b;
+  double* var;
+  int8_t* status;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256) schur_solve(SchurArgs s) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long npairs = (long long)s.cols * s.t;
+  if (idx >= npairs) return;
+  const int i = (int)(idx / s.t);
+  const int j = (int)(idx - (long long)i * s.t);
+  const int t = s.t;
+  const double* row = s.C + (long long)i * s.ldc;
+
+  double u[P];
+  double uv = 0.0, uu = 0.0;
+#pragma unroll
+  for (int f = 0; f < P; ++f) {
+    double acc = __ldg(row + f * t + j);
+#pragma unroll
+    for (int l = 0; l < f; ++l) acc -= __ldg(s.Lpk + (long long)(f * (f + 1) / 2 + l) * t + j) * u[l];
+    u[f] = acc / __ldg(s.Lpk + (long long)(f * (f + 1) / 2 + f) * t + j);
+    uu += u[f] * u[f];
+    uv += u[f] * __ldg(s.v + (long long)f * t + j);
+  }
+  const double r = __ldg(row + P * t + j);
+  const double c = __ldg(row + s.nsq + j);
+  const double sigma = c - uu;
+  const double scale = s.literal ? __ldg(s.s2 + j) : 1.0;
+
+  int8_t st = 0;
+  if (!(isfinite(sigma) && isfinite(c) && isfinite(r) && isfinite(uv))) st = 2;
+  else if (!(sigma > s.eps_collinear * c)) st = 1;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  double bg = nan, vg = nan;
+  if (st == 0) {
+    bg = (r - uv) / sigma;
+    vg = scale / sigma;
+    if (!(isfinite(bg) && isfinite(vg))) { st = 2; bg = vg = nan; }
+  }
+  s.status[idx] = st;
+  if (!s.full) {
+    s.b[idx] = bg;
+    s.var[idx] = vg;
+    return;
+  }
+  // full mode: q = L^-T u (back substitution), then the X_L coefficients
+  double q[P];
+#pragma unroll
+  for (int f = P - 1; f >= 0; --f) {
+    double acc = u[f];
+#pragma unroll
+    for (int l = f + 1; l < P; ++l) acc -= __ldg(s.Lpk + (long long)(l * (l + 1) / 2 + f) * t + j) * q[l];
+    q[f] = acc / __ldg(s.Lpk + (long long)(f * (f + 1) / 2 + f) * t + j);
+  }
+  double* bo = s.b + idx * (P + 1);
+  double* vo = s.var + idx * (P + 1);
+#pragma unroll
+  for (int f = 0; f < P; ++f) {
+    if (st == 0) {
+      bo[f] = __ldg(s.betaT + (long long)f * t + j) - q[f] * bg;
+      vo[f] = scale * (__ldg(s.dinv + (long long)f * t + j) + q[f] * q[f] / sigma);
+    } else {
+      bo[f] = nan;
+      vo[f] = nan;
+    }
+  }
+  bo[P] = bg;
+  vo[P] = vg;
+}
+
+}  // namespace gw

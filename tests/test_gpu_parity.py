@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path through the C-ABI (libgwas.so) vs the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): max |b_gpu - b_ref| / SE_ref <= 1e-8, max Var relative error <= 1e-8,
+statuses identical.  Invariance checks (block size, input placement, X_R dtype, trait slicing) are bitwise.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from gpu_helpers import TOL_B, TOL_VAR, compare
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _gw():
+    import paper_1207_2169_b200 as gw
+    return gw
+
+
+def _ld(n, es=1):
+    q = 16 // es
+    return (n + q - 1) // q * q
+
+
+def _run(cfg, ds, XR, **kw):
+    gw = _gw()
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, **kw)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    b, v, s = eng.run(XR)
+    torch.cuda.synchronize()
+    out = b.cpu().numpy(), v.cpu().numpy(), s.cpu().numpy()
+    eng.close()
+    return out
+
+
+@pytest.fixture(scope="module")
+def c0():
+    cfg = datagen.CONFIGS[0]
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    return cfg, ds, XR, ref
+
+
+# ------------------------------------------------------------------ K1/K2 kernel unit checks
+@pytest.mark.parametrize("M,N,K,u8,nsq", [(300, 200, 1000, True, None), (129, 131, 17, False, None),
+                                          (1, 8, 16, False, None), (257, 300, 333, False, 160),
+                                          (8192, 136, 1000, True, None), (64, 500, 4096, False, 248)])
+def test_gemm_kernel_vs_fp64_reference(M, N, K, u8, nsq):
+    gw = _gw()
+    rng = np.random.default_rng(M * 7 + N)
+    if u8:
+        A = rng.integers(0, 3, size=(M, _ld(K, 1)), dtype=np.uint8)
+    else:
+        A = rng.standard_normal((M, _ld(K, 8)))
+    B = rng.standard_normal((N, _ld(K, 8)))
+    Ct = gw.gemm_tn(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), nsq=nsq, K=K).cpu().numpy()
+    Af = A[:, :K].astype(np.float64)
+    Bf = B[:, :K]
+    ref = Af @ Bf.T
+    if nsq is not None:
+        ref[:, nsq:] = (Af * Af) @ Bf[nsq:].T
+        scale = (np.abs(Af) ** 2).max() * np.abs(Bf).max() * K
+    else:
+        scale = np.abs(Af).max() * np.abs(Bf).max() * K
+    err = np.max(np.abs(Ct - ref)) / scale
+    assert err <= 1e-15, err
+
+
+# ------------------------------------------------------------------ config 0: every pair
+def test_c0_all_pairs(c0):
+    cfg, ds, XR, ref = c0
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), block_cols=cfg.block_cols)
+    eb, ev = compare(b, v, s, ref)
+    print(f"C0 all {cfg.m * cfg.t} pairs: max|db|/SE={eb:.3e} max Var rel={ev:.3e}")
+    assert eb <= TOL_B and ev <= TOL_VAR
+
+
+def test_c0_full_output_mode(c0):
+    cfg, ds, XR, ref = c0
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), output_mode="full")
+    assert b.shape == (cfg.m, cfg.t, cfg.p + 1)
+    eb, ev = compare(b, v, s, ref, full=True)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+def test_c0_literal_var_convention(c0):
+    cfg, ds, XR, _ = c0
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:500, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2,
+                              var_convention=1)
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR[:500]).cuda(), var_convention="literal")
+    eb, ev = compare(b, v, s, ref)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+# ------------------------------------------------------------------ invariances (bitwise)
+def test_block_size_and_placement_invariance(c0):
+    cfg, ds, XR, _ = c0
+    dev = torch.from_numpy(XR).cuda()
+    base = _run(cfg, ds, dev, block_cols=2000)
+    for k in (512, 333, 8192, 1):
+        other = _run(cfg, ds, dev[:600] if k == 1 else dev, block_cols=k)
+        for x, y in zip(base, other):
+            np.testing.assert_array_equal(x[: y.shape[0]], y)
+    # pinned host input: 1-D staging copy (ld % 16 == 0) and 2-D staging copy (ld = n)
+    host_pad = torch.from_numpy(XR).pin_memory()
+    host_n = torch.from_numpy(np.ascontiguousarray(XR[:, :cfg.n])).pin_memory()
+    for src in (host_pad, host_n):
+        other = _run(cfg, ds, src, block_cols=700)
+        for x, y in zip(base, other):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_f64_dosages_equal_u8(c0):
+    cfg, ds, XR, _ = c0
+    base = _run(cfg, ds, torch.from_numpy(XR).cuda())
+    XRf = torch.from_numpy(XR[:, :cfg.n].astype(np.float64)).cuda()  # ld = n = 200 (even): 16-byte rows
+    other = _run(cfg, ds, XRf, xr_dtype="f64")
+    for x, y in zip(base, other):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_trait_slice_equals_single_trait(c0):
+    cfg, ds, XR, _ = c0
+    dev = torch.from_numpy(XR).cuda()
+    full = _run(cfg, ds, dev)
+    j = 2
+    cfg1 = datagen.custom_config(n=cfg.n, p=cfg.p, m=cfg.m, t=1)
+    ds1 = datagen.Dataset(cfg1, ds.Phi, ds.XL, np.asfortranarray(ds.Y[:, [j]]), ds.h2[[j]], ds.s2[[j]])
+    one = _run(cfg1, ds1, dev)
+    np.testing.assert_array_equal(full[0][:, j], one[0][:, 0])
+    np.testing.assert_array_equal(full[1][:, j], one[1][:, 0])
+
+
+# ------------------------------------------------------------------ ragged shapes, edge cases
+@pytest.mark.parametrize("n,p,t,m,k", [(333, 3, 37, 777, 256), (17, 2, 1, 40, 16), (129, 6, 9, 300, 300),
+                                       (250, 1, 3, 130, 64)])
+def test_ragged_shapes_f64(n, p, t, m, k):
+    cfg = datagen.custom_config(n=n, p=p, m=m, t=t, index=200 + n)
+    ds = datagen.dataset(cfg)
+    G = datagen.xr_dosages(cfg).astype(np.float64)
+    ld = _ld(n, 8)
+    XR = np.zeros((m, ld))
+    XR[:, :n] = G
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, G.T, ds.Y, ds.h2, ds.s2)
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), xr_dtype="f64", block_cols=k, output_mode="full")
+    eb, ev = compare(b, v, s, ref, full=True)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+def test_collinear_and_nonfinite_pairs():
+    cfg = datagen.custom_config(n=120, p=4, m=50, t=3, index=301)
+    ds = datagen.dataset(cfg)
+    G = datagen.xr_dosages(cfg).astype(np.float64)
+    G[0] = 1.0                      # monomorphic: a multiple of the intercept
+    G[1] = 3.0 * ds.XL[:, 1]        # copy of a covariate
+    G[2] = 2.0 * ds.XL[:, -1]       # copy of the sex column
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, G.T, ds.Y, ds.h2, ds.s2)
+    assert (ref["status"][:3] == oracle.STATUS_COLLINEAR).all()
+    G2 = G.copy()
+    G2[3, 7] = np.nan               # non-finite dosage
+    b, v, s = _run(cfg, ds, torch.from_numpy(G2).cuda(), xr_dtype="f64")
+    assert (s[:3] == 1).all() and (s[3] == 2).all() and (s[4:] == 0).all()
+    assert np.isnan(b[:4]).all() and np.isnan(v[:4]).all()
+    eb, ev = compare(b[4:], v[4:], s[4:], {k: (x[4:] if k != "traits" else x) for k, x in ref.items()})
+    assert eb <= TOL_B and ev <= TOL_VAR
+
+
+def test_empty_and_single_column(c0):
+    cfg, ds, XR, ref = c0
+    gw = _gw()
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    dev = torch.from_numpy(XR).cuda()
+    b, v, s = eng.run(dev[:0])
+    assert b.shape == (0, cfg.t)
+    b, v, s = eng.run(dev[5:6])
+    torch.cuda.synchronize()
+    eb, ev = compare(b.cpu().numpy(), v.cpu().numpy(), s.cpu().numpy(),
+                     {k: (x[5:6] if k != "traits" else x) for k, x in ref.items()})
+    assert eb <= TOL_B and ev <= TOL_VAR
+    eng.close()
+
+
+def test_setup_errors():
+    gw = _gw()
+    cfg = datagen.custom_config(n=64, p=3, m=10, t=2, index=302)
+    ds = datagen.dataset(cfg)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0)
+    with pytest.raises(gw.GwasError) as e:
+        eng.setup(ds.Phi, ds.XL, ds.Y, np.array([0.5, 1.5]), ds.s2)
+    assert e.value.code == 1 and "h2[1]" in str(e.value)
+    with pytest.raises(gw.GwasError) as e:
+        eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, np.array([1.0, 0.0]))
+    assert e.value.code == 1
+    XL = ds.XL.copy()
+    XL[:, 2] = XL[:, 1]
+    with pytest.raises(gw.GwasError) as e:
+        eng.setup(ds.Phi, XL, ds.Y, ds.h2, ds.s2)
+    assert e.value.code == 2 and "trait 0" in str(e.value)
+    # h2 = 1 with the (singular, Phi 1 = 0) sample-centred GRM: D_j has a non-positive denominator (reading A7)
+    with pytest.raises(gw.GwasError) as e:
+        eng.setup(ds.Phi, ds.XL, ds.Y, np.array([0.3, 1.0]), ds.s2)
+    assert e.value.code == 2 and "trait 1" in str(e.value)
+    with pytest.raises(gw.GwasError):
+        gw.Gwas(3, 5, 1)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)  # a failed setup leaves the engine usable
+    with pytest.raises(gw.GwasError) as e:        # pageable host X_R is refused (would serialise staging)
+        import paper_1207_2169_b200._lib as L
+        XR = np.zeros((4, 64), dtype=np.uint8)
+        b, v, s = eng.alloc_outputs(4)
+        L.check(L.lib.gwas_run(eng._ctx, 4, XR.ctypes.data, 64, b.data_ptr(), v.data_ptr(), s.data_ptr()))
+    assert e.value.code == 1
+    eng.close()
+
+
+def test_attach_after_state_copy(c0):
+    """Multi-GPU replication path on one device: a second context attaches to a byte copy of the state."""
+    cfg, ds, XR, _ = c0
+    gw = _gw()
+    a = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0)
+    a.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    bcopy = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0)
+    bcopy.state.copy_(a.state)
+    bcopy.attach()
+    dev = torch.from_numpy(XR).cuda()
+    r1 = [x.cpu().numpy() for x in a.run(dev)]
+    r2 = [x.cpu().numpy() for x in bcopy.run(dev)]
+    for x, y in zip(r1, r2):
+        np.testing.assert_array_equal(x, y)
+    wrong = gw.Gwas(cfg.n, cfg.p, cfg.t + 1, device=0)
+    with pytest.raises(gw.GwasError) as e:
+        wrong.attach()
+    assert e.value.code in (6,)
