@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native CLAK-Eig GLS-sequence hot path (BASELINE.json metric: GLS/s = SNP x trait pairs
+per second, with the FP64 tensor-pipe fraction of peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (one process per GPU, NCCL)
+
+A step = one pass of the whole hot path (Alg. 4 line 3 + lines 13-16: K1 rotation
+GEMM, K2 weighted-reduction GEMM, K3 Schur solve) over every SNP of the rank's shard, for all t traits.
+Setup (dsyevd, precompute, the one NCCL broadcast of the replicated state) is timed and reported separately.
+Scaling is weak: every rank processes its own m SNPs of the config (rank r takes SNP columns [r m, (r+1) m) of
+an N*m-SNP synthetic genome), so `value` = N*m*t / (max over ranks of the step time).
+
+`value`: X_R already resident in HBM (uint8 dosages, exact), timed with CUDA events on the compute stream.
+`e2e`:   the same through the public API from pinned HOST X_R (block staging on the copy stream inside the timed
+         region) plus the device->host read of every step's b, Var and status.
+`--impl reference`: the CPU oracle (oracle/), as it stands, on a bounded sample of the same workload (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+
+METRIC = "GLS/s (SNP x trait pairs)"
+UNIT = "GLS/s"
+
+
+# ------------------------------------------------------------------ host-side helpers (CPU-testable)
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def shard_range(m: int, rank: int, world: int, scaling: str = "weak"):
+    """SNP columns of a rank.  weak: [rank*m, (rank+1)*m) of an N*m genome; strong: contiguous split of m."""
+    if scaling == "weak":
+        return rank * m, (rank + 1) * m
+    return (rank * m) // world, ((rank + 1) * m) // world
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def flops_per_block(n, p, t, cols):
+    """Algorithmic flops: K1 2 n^2 k, K2 2 n k t (p+2); K3 ~ k t (p^2 + 4p + 8)."""
+    return {"K1": 2.0 * n * n * cols, "K2": 2.0 * n * cols * t * (p + 2), "K3": cols * t * (p * p + 4 * p + 8.0)}
+
+
+def k3_bytes(p, t, cols, full=False):
+    """K3 algorithmic HBM bytes: reads 8 (p+2) per pair, writes 8+8+1 (SNP mode) or 16 (p+1)+1 (full)."""
+    w = p + 1
+    return cols * t * (8 * (p + 2) + (16 * w + 1 if full else 17))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs."""
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                vals = [v.strip() for v in out.strip().split(",")]
+                if len(vals) >= 8:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._loop, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
+
+
+def fp64_peak():
+    """Measured FP64 DMMA peak (tools/fp64_peak.cu on this pool's B200: back-to-back mma.sync.m8n8k4.f64 on all
+    SMs, profiles/fp64_peak_r01.json).  MEASURED_PEAKS.json has no FP64 entry."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    with open(path) as f:
+        d = json.load(f)
+    return float(d["dmma_tflops"]), "measured: tools/fp64_peak.cu DMMA.8x8x4 microbenchmark (profiles/fp64_peak_r01.json)"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return None
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------------ oracle (cpu_baseline / --impl reference)
+def oracle_sample(cfg, ds, traits, snps):
+    """Time the CPU oracle, as it stands, on (snps x traits) of the config.  Returns (pairs, seconds, threads)."""
+    import scipy.linalg  # noqa: F401  (loads the LAPACK the oracle uses)
+    import threadpoolctl
+
+    import oracle
+    G = datagen.xr_columns(cfg, snps)
+    t0 = time.perf_counter()
+    oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
+    dt = time.perf_counter() - t0
+    info = threadpoolctl.threadpool_info()
+    threads = max([i.get("num_threads", 1) for i in info] or [1])
+    return len(snps) * len(traits), dt, threads
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1207_2169_b200 as gw
+
+    cfg = datagen.CONFIGS[args.config]
+    m_rank = cfg.m if args.snps is None else args.snps
+    lo, hi = shard_range(m_rank, rank, world, args.scaling)
+    if args.scaling == "weak":
+        gcfg = datagen.Config(cfg.index, cfg.n, cfg.p, m_rank * world, cfg.t, cfg.S, cfg.h2_range, cfg.s2_range)
+    else:
+        gcfg = datagen.Config(cfg.index, cfg.n, cfg.p, m_rank, cfg.t, cfg.S, cfg.h2_range, cfg.s2_range)
+    ncols = hi - lo
+    n, p, t = cfg.n, cfg.p, cfg.t
+    ld = (n + 15) // 16 * 16
+
+    # inputs: the replicated part on every rank (deterministic), X_R shard in pinned host memory
+    t0 = time.perf_counter()
+    ds = datagen.dataset(cfg, device=dev)
+    xr_host = torch.empty((ncols, ld), dtype=torch.uint8, pin_memory=True)
+    datagen.xr_dosages(gcfg, lo, hi, ld=ld, out=xr_host.numpy())
+    t_gen = time.perf_counter() - t0
+
+    eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True)
+    setup = {}
+    if rank == 0:
+        eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+        setup.update(eng.timings())
+    if world > 1:
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dist.broadcast(eng.state, src=0)          # the one collective: replicated setup state over NVLink
+        e1.record()
+        torch.cuda.synchronize(dev)
+        setup["ms_broadcast"] = e0.elapsed_time(e1)
+        setup["broadcast_bytes"] = eng.state_bytes
+        if rank != 0:
+            eng.attach()
+
+    xr_dev = xr_host.to(dev)
+    out = eng.alloc_outputs(ncols)
+    stream = eng.compute_stream
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- device-resident timed region (value)
+    for _ in range(args.warmup):
+        eng.run(xr_dev, out=out)
+    barrier()
+    eng.kernel_times(reset=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            eng.run(xr_dev, out=out)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    kt = eng.kernel_times(reset=True)
+    ms_max = max_over_ranks(ms, world, dev)
+    pairs_total = float(ncols) * t * world if args.scaling == "weak" else float(m_rank) * t
+    value = pairs_total * args.steps / (ms_max / 1e3)
+
+    # ---------------- end-to-end through the public API from pinned host memory (e2e)
+    b_h = torch.empty(out[0].shape, dtype=torch.float64, pin_memory=True)
+    v_h = torch.empty(out[1].shape, dtype=torch.float64, pin_memory=True)
+    s_h = torch.empty(out[2].shape, dtype=torch.int8, pin_memory=True)
+
+    def e2e_step():
+        b, v, s = eng.run(xr_host, out=out)
+        with torch.cuda.stream(stream):
+            b_h.copy_(b, non_blocking=True)
+            v_h.copy_(v, non_blocking=True)
+            s_h.copy_(s, non_blocking=True)
+
+    e2e_steps = max(1, args.e2e_steps)
+    e2e_step()
+    barrier()
+    eng.kernel_times(reset=True)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1), world, dev)
+    kt_e2e = eng.kernel_times(reset=True)
+    e2e_value = pairs_total * e2e_steps / (ms_e2e / 1e3)
+    h2d = ncols * n * 1  # uint8 dosages actually copied (n of ld bytes per column... 1-D copy moves ld)
+    h2d = (ncols - 1) * ld + n
+    d2h = b_h.numel() * 8 + v_h.numel() * 8 + s_h.numel()
+
+    # ---------------- parity spot check on this run's outputs (outside timed regions)
+    parity = None
+    if args.check and rank == 0:
+        parity = spot_check(cfg, gcfg, ds, lo, hi, b_h.numpy(), v_h.numpy(), s_h.numpy(), args.check)
+
+    # ---------------- roofline of the dominant kernel (K1) and the GEMM stages
+    blocks = [min(args.block, ncols - c) for c in range(0, ncols, args.block)]
+    fl = [flops_per_block(n, p, t, c) for c in blocks]
+    k1_flops = sum(f["K1"] for f in fl) * args.steps
+    k2_flops = sum(f["K2"] for f in fl) * args.steps
+    peak, peak_src = fp64_peak()
+    k1_ms = kt["K1"]["ms"]
+    k2_ms = kt["K2"]["ms"]
+    k3_ms = kt["K3"]["ms"]
+    k1_tf = k1_flops / (k1_ms / 1e3) / 1e12
+    k2_tf = k2_flops / (k2_ms / 1e3) / 1e12
+    gemm_tf = (k1_flops + k2_flops) / ((k1_ms + k2_ms) / 1e3) / 1e12
+    k3_gbs = sum(k3_bytes(p, t, c) for c in blocks) * args.steps / (k3_ms / 1e3) / 1e9
+    traffic = ncu_traffic()
+    launches_per_step = 3 * len(blocks)
+
+    res = None
+    if rank == 0:
+        clocks = clk.summary()
+        res = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen, seeded)",
+            "config": {"workload": f"{cfg.name}: n={n}, p={p}, m={m_rank}/rank, t={t}, k={args.block}, "
+                                   f"X_R uint8 dosages resident in HBM",
+                       "n": n, "p": p, "m_per_rank": ncols, "t": t, "block_cols": args.block,
+                       "pairs_per_step": pairs_total, "parallelism": f"snp-shard x{world}",
+                       "l2": "inputs larger than L2 (Z 0.8 GB, X_R 10 GB at C4); no flush"},
+            "roofline": {"bound": "tensor", "kernel": "K1 rotation GEMM (FP64 DMMA)", "achieved": k1_tf,
+                         "peak": peak, "unit": "TFLOP/s", "frac": k1_tf / peak,
+                         "traffic": (traffic or {}).get("bytes_per_launch"),
+                         "algorithmic_flops_per_launch": 2.0 * n * n * args.block,
+                         "avg_launch_ms": k1_ms / max(1, kt["K1"]["launches"]), "peak_source": peak_src},
+            "gemm_stages": {"K1_tflops": k1_tf, "K2_tflops": k2_tf, "K1K2_tflops": gemm_tf,
+                            "K1K2_frac_of_peak": gemm_tf / peak, "K3_hbm_gbs": k3_gbs,
+                            "share_of_step": {k: kt[k]["ms"] / ms for k in ("K1", "K2", "K3")}},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps, "ms_per_step": ms_e2e / e2e_steps,
+                    "h2d_ms_per_step": kt_e2e["H2D"]["ms"] / e2e_steps},
+            "gpu_launches": launches_per_step * args.steps,
+            "setup": {**setup, "datagen_s": t_gen},
+            "clocks": clocks,
+        }
+        if parity is not None:
+            res["parity"] = parity
+        if not args.no_cpu_baseline:
+            pairs, sec, thr = cpu_baseline_sample(cfg, ds, args)
+            res["cpu_baseline"] = {"value": pairs / sec, "unit": UNIT, "cores": thr, "kind": "oracle",
+                                   "sample": f"{pairs} pairs of {cfg.name} ({args.cpu_traits} traits x "
+                                             f"{args.cpu_snps} SNPs, Alg. 1 per problem, fp64 numpy/LAPACK), "
+                                             f"{sec:.1f} s on {host_cores()} host cores"}
+    eng.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return res
+
+
+def cpu_baseline_sample(cfg, ds, args):
+    rng = np.random.default_rng(cfg.seed)
+    traits = np.sort(rng.choice(cfg.t, size=min(cfg.t, args.cpu_traits), replace=False))
+    snps = np.sort(rng.choice(cfg.m, size=min(cfg.m, args.cpu_snps), replace=False))
+    return oracle_sample(cfg, ds, traits, snps)
+
+
+def spot_check(cfg, gcfg, ds, lo, hi, b, v, s, npairs):
+    """Oracle on a seeded sample of this rank's pairs (after the timed regions)."""
+    import oracle
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from gpu_helpers import compare
+    rng = np.random.default_rng(cfg.seed + 1)
+    nt = min(cfg.t, 4)
+    traits = np.sort(rng.choice(cfg.t, size=nt, replace=False))
+    ns = max(1, npairs // nt)
+    loc = np.unique(np.concatenate([[0, hi - lo - 1], rng.choice(hi - lo, size=min(ns, hi - lo), replace=False)]))
+    G = datagen.xr_columns(gcfg, loc + lo)
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
+    eb, ev = compare(b[np.ix_(loc, traits)], v[np.ix_(loc, traits)], s[np.ix_(loc, traits)], ref)
+    return {"pairs": int(loc.size * nt), "max_db_over_se": eb, "max_var_rel": ev, "tol": 1e-8,
+            "pass": bool(eb <= 1e-8 and ev <= 1e-8)}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return None
+    cfg = datagen.CONFIGS[args.config]
+    dev = None
+    try:
+        import torch
+        if torch.cuda.is_available():
+            dev = torch.device("cuda", local)
+    except Exception:
+        pass
+    ds = datagen.dataset(cfg, device=dev)
+    rng = np.random.default_rng(cfg.seed + 7)
+    times, pairs_all, thr = [], 0, 1
+    for step in range(args.warmup + args.steps):
+        traits = np.array([int(rng.integers(cfg.t))])
+        snps = np.sort(rng.choice(cfg.m, size=min(cfg.m, args.ref_snps), replace=False))
+        pairs, sec, thr = oracle_sample(cfg, ds, traits, snps)
+        if step >= args.warmup:
+            times.append(sec)
+            pairs_all += pairs
+    total = sum(times)
+    value = pairs_all / total
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen, seeded)",
+            "impl": "reference",
+            "config": {"workload": f"{cfg.name}: n={cfg.n}, p={cfg.p}, m={cfg.m}, t={cfg.t} -- per step a bounded "
+                                   f"sample: 1 trait x {args.ref_snps} SNPs", "n": cfg.n, "p": cfg.p, "t": cfg.t},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                             "sample": f"per step 1 trait x {args.ref_snps} SNPs of {cfg.name}; "
+                                       f"{host_cores()} host cores"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4, help="BASELINE.json config index (default 4)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--block", type=int, default=8192, help="SNP columns per streamed block (k)")
+    ap.add_argument("--snps", type=int, default=None, help="override m per rank (testing only)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--check", type=int, default=2000, help="oracle spot-check pairs after timing (0 = off)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-traits", type=int, default=4)
+    ap.add_argument("--cpu-snps", type=int, default=1024)
+    ap.add_argument("--ref-snps", type=int, default=64)
+    args = ap.parse_args(argv)
+    rank, world, _ = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None and rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

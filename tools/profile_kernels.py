@@ -1,0 +1,25 @@
+"""One block of K1 -> K2 -> K3 at a config's full n, p, t (for ncu captures).  Not product code.
+    python tools/profile_kernels.py --config 4 [--cols 8192] [--reps 1]"""
+import argparse, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import datagen
+import paper_1207_2169_b200 as gw
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--cols", type=int, default=8192)
+ap.add_argument("--reps", type=int, default=1)
+a = ap.parse_args()
+cfg = datagen.CONFIGS[a.config]
+ld = (cfg.n + 15) // 16 * 16
+ds = datagen.dataset(cfg, device="cuda")
+XR = torch.from_numpy(datagen.xr_dosages(cfg, 0, a.cols, ld=ld)).cuda()
+eng = gw.Gwas(cfg.n, cfg.p, cfg.t, block_cols=a.cols, timing=True)
+eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+out = eng.alloc_outputs(a.cols)
+for _ in range(a.reps):
+    eng.run(XR, out=out)
+torch.cuda.synchronize()
+print(eng.kernel_times())
