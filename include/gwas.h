@@ -132,7 +132,7 @@ GWAS_API gwas_status gwas_kernel_times(gwas_ctx* ctx, double* ms, int64_t* launc
 /* Unit-test entry to the K1/K2 kernel itself (no context):  C[i][c] = sum_r A(r, i) * B(r, c) for
  * i < M, c < N, r < K, with A column-major K x M (ld lda; uint8 if a_u8 else fp64) and B column-major K x N
  * (ld ldb), C row-major M x N (ld ldc); columns c >= nsq use A(r,i)^2 (K2's squared block; pass
- * nsq >= N for a plain product).  All device pointers; lda*elem and ldb*8 multiples of 16, ldc even. */
+ * nsq >= N for a plain product; otherwise nsq % 32 == 0).  All device pointers; lda*elem and ldb*8 multiples of 16, ldc even. */
 GWAS_API gwas_status gwas_gemm_tn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int32_t a_u8,
                          const double* B, int64_t ldb, double* C, int64_t ldc, int64_t nsq, void* stream);
 

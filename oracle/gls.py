@@ -30,7 +30,8 @@ fused or reordered beyond that; no eigendecomposition appears anywhere in the or
 
 Collinearity (reading A6): in step 7 the last pivot R_ww^2 of S equals the Schur complement of the SNP
 column; if R_ww^2 <= eps_collinear * S_ww the pair gets status 1 and NaN payload (the paper is silent).
-Any earlier pivot <= 0 means X_L itself is rank-deficient -> ValueError (the GPU path's GWAS_E_NOT_SPD).
+The same relative test on an earlier pivot (R_kk^2 <= eps_collinear * S_kk, k < w-1) means X_L itself is
+rank-deficient -> ValueError (the GPU path's GWAS_E_NOT_SPD).
 
 Pins: tests/test_oracle.py (P1-P10, P12 of SURVEY.md §8(c)).  No function here is
 "parity unpinned".
@@ -105,7 +106,8 @@ def _finish(S, r, sigma2, eps_collinear, var_convention):
     Returns b (..., w), Var (..., w, w), status (...)."""
     w = S.shape[-1]
     R, piv = small_cholesky(S)
-    if np.any(piv[..., : w - 1] <= 0):
+    diag = np.diagonal(S, axis1=-2, axis2=-1)
+    if np.any(~(piv[..., : w - 1] > eps_collinear * diag[..., : w - 1])):
         raise ValueError("S_TL not SPD: X_L is rank-deficient for some trait")
     last = piv[..., w - 1]
     collinear = ~(last > eps_collinear * S[..., w - 1, w - 1])

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace gw {
 
 constexpr int GEMM_BK = 16;                 // K elements per stage (one 128-byte fp64 row)
@@ -128,7 +130,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   using L = GemmSmem<TA, BM, BN>;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment for the 128B-swizzled TMA tiles, by pointer offset (keeps the shared address space
+  // visible to the compiler, so fragment reads are LDS, not generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;
   uint8_t* sA = sB + STAGES * L::kBStride;
   uint64_t* full = reinterpret_cast<uint64_t*>(sA + STAGES * L::kAStride);
@@ -189,48 +193,63 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // K2: which of this warp's 8-column fragments take the squared A operand (nsq is a multiple of 8)
-  bool sq[NI];
-  bool any_sq = false;
-#pragma unroll
-  for (int j = 0; j < NI; ++j) {
-    sq[j] = SQ && (n0 + wn * WN + j * 8 >= s.nsq);
-    any_sq |= sq[j];
-  }
+  // K2: this warp's 32 columns take the squared A operand iff they lie in the D block (nsq % 32 == 0)
+  const bool warp_sq = SQ && (n0 + wn * WN >= s.nsq);
 
-  for (int kt = 0; kt < KT; ++kt) {
-    const int st = kt % STAGES;
-    if (threadIdx.x == 0 && kt >= 1 && kt + STAGES - 2 < KT) produce(kt + STAGES - 2);
-    __syncwarp();
-    mbar_wait(&full[st], (kt / STAGES) & 1);
-    const uint8_t* a_tile = sA + st * L::kAStride;
-    const uint8_t* b_tile = sB + st * L::kBStride;
+  // K order inside a 16-wide stage: mma step ks, lane quad-index q reads k = 2 ks + (q & 1) + 8 (q >> 1).
+  // Any bijection is valid (A and B use the same one); this one makes every half-warp's 16 64-bit fragment reads
+  // hit 16 distinct 8-byte slots of the 128B-swizzled rows (the natural k = 4 ks + q is 2-way bank-conflicted).
+  uint32_t off_f64[GEMM_BK / 4], off_u8[GEMM_BK / 4];
 #pragma unroll
-    for (int ks = 0; ks < GEMM_BK / 4; ++ks) {
-      const int k = ks * 4 + q;
-      double a[MI], b[NI];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = load_a<TA>(a_tile, lut, wm * WM + i * 8 + g, k);
-#pragma unroll
-      for (int j = 0; j < NI; ++j) b[j] = *reinterpret_cast<const double*>(b_tile + swz128_off(wn * WN + j * 8 + g, k));
-      if (SQ && any_sq) {
-        double a2[MI];
-#pragma unroll
-        for (int i = 0; i < MI; ++i) a2[i] = a[i] * a[i];
-#pragma unroll
+  for (int ks = 0; ks < GEMM_BK / 4; ++ks) {
+    const int k = 2 * ks + (q & 1) + 8 * (q >> 1);
+    off_f64[ks] = swz128_off(g, k);
+    off_u8[ks] = (uint32_t)(g * GEMM_BK + k);
+  }
+  const uint32_t a_row0 = (uint32_t)(wm * WM) * ATile<TA>::kBytesPerRow;
+  const uint32_t b_row0 = (uint32_t)(wn * WN) * (GEMM_BK * 8);
+
+  // The mainloop is instantiated twice so the K2 squaring is a warp-uniform choice made once, outside the loop
+  // (a per-iteration branch compiles to predicated DMULs that still occupy the shared FP64/DMMA dispatch).
+  auto mainloop = [&](auto square_tag) {
+    constexpr bool SQUARE = decltype(square_tag)::value;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % STAGES;
+      if (threadIdx.x == 0 && kt >= 1 && kt + STAGES - 2 < KT) produce(kt + STAGES - 2);
+      __syncwarp();
+      mbar_wait(&full[st], (kt / STAGES) & 1);
+      const uint8_t* a_tile = sA + st * L::kAStride + a_row0;
+      const uint8_t* b_tile = sB + st * L::kBStride + b_row0;
+  #pragma unroll
+      for (int ks = 0; ks < GEMM_BK / 4; ++ks) {
+        double a[MI], b[NI];
+  #pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          if constexpr (sizeof(TA) == 1) {
+            a[i] = lut[a_tile[off_u8[ks] + i * 8 * GEMM_BK]];
+          } else {
+            a[i] = *reinterpret_cast<const double*>(a_tile + off_f64[ks] + i * 8 * 128);
+          }
+        }
+  #pragma unroll
+        for (int j = 0; j < NI; ++j) b[j] = *reinterpret_cast<const double*>(b_tile + off_f64[ks] + j * 8 * 128);
+        if constexpr (SQUARE) {
+  #pragma unroll
+          for (int i = 0; i < MI; ++i) a[i] = a[i] * a[i];
+        }
+  #pragma unroll
         for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j], sq[j] ? a2[i] : a[i], b[j]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
+  #pragma unroll
           for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
+  };
+  if (SQ && warp_sq)
+    mainloop(std::true_type{});
+  else
+    mainloop(std::false_type{});
 
   // ---------------- epilogue: each lane owns C[row][2q, 2q+1] of every 8x8 fragment
 #pragma unroll

@@ -81,7 +81,7 @@ Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   d.p = p;
   d.t = t;
   d.kpad = round_up(n, 16);
-  d.nsq = round_up(t * (p + 1), 8);
+  d.nsq = round_up(t * (p + 1), 32);
   d.n2 = d.nsq + t;
   d.ldc2 = round_up(d.n2, 2);
   d.lds = round_up(t * (p + 1), 2);
@@ -273,7 +273,7 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.tiles_n = (int)((N + kBN - 1) / kBN);
   s.group_m = 16;
   const bool sq = nsq < N;
-  if (sq && (nsq % 8)) return fail(GWAS_E_ARG, "nsq must be a multiple of 8");
+  if (sq && (nsq % 32)) return fail(GWAS_E_ARG, "nsq must be a multiple of 32");
   if (a_u8) {
     if (sq) return launch_gemm_t<uint8_t, kStagesU8, true>(ma, mb, s, st);
     return launch_gemm_t<uint8_t, kStagesU8, false>(ma, mb, s, st);
@@ -545,7 +545,8 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     }
     // Alg. 4 lines 10-11: S_TL_j = X_L'^T D_j X_L', b_T_j = X_L'^T D_j y'_j for all j (K2 kernel)
     CKG(gemm_tn(false, xlp, d.kpad, c->B2(), d.kpad, stl, d.lds, p, t * (p + 1), n, d.n2, cs));
-    gw::trait_factor<kPMax><<<(unsigned)((t + 127) / 128), 128, 0, cs>>>(stl, d.lds, (int)p, (int)t, c->Lpk(), c->v(),
+    gw::trait_factor<kPMax><<<(unsigned)((t + 127) / 128), 128, 0, cs>>>(stl, d.lds, (int)p, (int)t,
+                                                                         o->eps_collinear, c->Lpk(), c->v(),
                                                                          c->betaT(), c->dinv(), derr + 1);
     CKC(cudaGetLastError());
     CKC(cudaEventRecord(e3, cs));

@@ -45,9 +45,9 @@ __global__ void build_b2(const double* __restrict__ XLp, const double* __restric
 // Alg. 4 lines 10-11 finished per trait: S_TL_j[f][l] = STL[f][l t + j], b_T_j[f] = STL[f][p t + j]
 // (both produced by K2 with A = X_L'^T).  Cholesky S_TL_j = L L^T (lower triangle of S_TL read), v = L^-1 b_T,
 // and for the full output mode betaT = S_TL^-1 b_T = L^-T v and dinv = diag(S_TL^-1) = column sums of L^-1 squared.
-// A non-positive pivot (X_L rank-deficient) records the smallest such j in *err.
+// A pivot <= eps_rel * S_kk (X_L rank-deficient, reading A6) records the smallest such j in *err.
 template <int PMAX>
-__global__ void trait_factor(const double* __restrict__ STL, long long lds, int p, int t,
+__global__ void trait_factor(const double* __restrict__ STL, long long lds, int p, int t, double eps_rel,
                              double* __restrict__ Lpk, double* __restrict__ v, double* __restrict__ betaT,
                              double* __restrict__ dinv, unsigned long long* err) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -60,9 +60,11 @@ __global__ void trait_factor(const double* __restrict__ STL, long long lds, int 
   }
   bool ok = true;
   for (int k = 0; k < p; ++k) {
-    double d = L[k][k];
+    const double skk = L[k][k];
+    double d = skk;
     for (int l = 0; l < k; ++l) d -= L[k][l] * L[k][l];
-    if (!(d > 0.0) || !isfinite(d)) { ok = false; d = 1.0; }
+    // relative pivot test (reading A6 applied to X_L): a column of X_L' numerically in the span of the others
+    if (!(d > eps_rel * skk) || !isfinite(d)) { ok = false; d = 1.0; }
     const double rkk = sqrt(d);
     L[k][k] = rkk;
     for (int i = k + 1; i < p; ++i) {
