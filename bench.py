@@ -64,6 +64,15 @@ def max_over_ranks(x: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def replicate_state(state, world: int, src: int = 0):
+    """Alg. 4's per-trait precomputation is done once on rank `src`; every other rank receives the state bytes
+    (Z, W, B_op/D, per-trait factors) through ONE broadcast -- the only collective of the method."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast(state, src=src)
+    return state
+
+
 def flops_per_block(n, p, t, cols):
     """Algorithmic flops: K1 2 n^2 k, K2 2 n k t (p+2); K3 ~ k t (p^2 + 4p + 8)."""
     return {"K1": 2.0 * n * n * cols, "K2": 2.0 * n * cols * t * (p + 2), "K3": cols * t * (p * p + 4 * p + 8.0)}
@@ -200,7 +209,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        dist.broadcast(eng.state, src=0)          # the one collective: replicated setup state over NVLink
+        replicate_state(eng.state, world)        # the one collective: replicated setup state over NVLink
         e1.record()
         torch.cuda.synchronize(dev)
         setup["ms_broadcast"] = e0.elapsed_time(e1)

@@ -209,39 +209,58 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t a_row0 = (uint32_t)(wm * WM) * ATile<TA>::kBytesPerRow;
   const uint32_t b_row0 = (uint32_t)(wn * WN) * (GEMM_BK * 8);
 
+  // Fragment loads for mma step ks of a stage (A through the u8 -> f64 table or directly; B always f64).
+  auto load_frags = [&](double (&a)[MI], double (&b)[NI], int st, int ks) {
+    const uint8_t* a_tile = sA + st * L::kAStride + a_row0;
+    const uint8_t* b_tile = sB + st * L::kBStride + b_row0;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      if constexpr (sizeof(TA) == 1) {
+        a[i] = lut[a_tile[off_u8[ks] + i * 8 * GEMM_BK]];
+      } else {
+        a[i] = *reinterpret_cast<const double*>(a_tile + off_f64[ks] + i * 8 * 128);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NI; ++j) b[j] = *reinterpret_cast<const double*>(b_tile + off_f64[ks] + j * 8 * 128);
+  };
+
   // The mainloop is instantiated twice so the K2 squaring is a warp-uniform choice made once, outside the loop
   // (a per-iteration branch compiles to predicated DMULs that still occupy the shared FP64/DMMA dispatch).
+  // Fragments are register double-buffered one mma step ahead, across stage boundaries too: the first step of
+  // stage kt+1 is loaded (after its full-barrier wait) while the last step of stage kt is in the DMMA pipe.
   auto mainloop = [&](auto square_tag) {
     constexpr bool SQUARE = decltype(square_tag)::value;
+    auto mma_step = [&](double (&a)[MI], double (&b)[NI]) {
+      if constexpr (SQUARE) {
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[i] = a[i] * a[i];
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+    };
+    static_assert(GEMM_BK / 4 == 4, "the step schedule below assumes 4 mma steps per stage");
+    double a0[MI], b0[NI], a1[MI], b1[NI];
+    mbar_wait(&full[0], 0);
+    load_frags(a0, b0, 0, 0);
     for (int kt = 0; kt < KT; ++kt) {
       const int st = kt % STAGES;
       if (threadIdx.x == 0 && kt >= 1 && kt + STAGES - 2 < KT) produce(kt + STAGES - 2);
       __syncwarp();
-      mbar_wait(&full[st], (kt / STAGES) & 1);
-      const uint8_t* a_tile = sA + st * L::kAStride + a_row0;
-      const uint8_t* b_tile = sB + st * L::kBStride + b_row0;
-  #pragma unroll
-      for (int ks = 0; ks < GEMM_BK / 4; ++ks) {
-        double a[MI], b[NI];
-  #pragma unroll
-        for (int i = 0; i < MI; ++i) {
-          if constexpr (sizeof(TA) == 1) {
-            a[i] = lut[a_tile[off_u8[ks] + i * 8 * GEMM_BK]];
-          } else {
-            a[i] = *reinterpret_cast<const double*>(a_tile + off_f64[ks] + i * 8 * 128);
-          }
-        }
-  #pragma unroll
-        for (int j = 0; j < NI; ++j) b[j] = *reinterpret_cast<const double*>(b_tile + off_f64[ks] + j * 8 * 128);
-        if constexpr (SQUARE) {
-  #pragma unroll
-          for (int i = 0; i < MI; ++i) a[i] = a[i] * a[i];
-        }
-  #pragma unroll
-        for (int i = 0; i < MI; ++i)
-  #pragma unroll
-          for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+      load_frags(a1, b1, st, 1);
+      mma_step(a0, b0);
+      load_frags(a0, b0, st, 2);
+      mma_step(a1, b1);
+      load_frags(a1, b1, st, 3);
+      mma_step(a0, b0);
+      if (kt + 1 < KT) {
+        const int nst = (kt + 1) % STAGES;
+        mbar_wait(&full[nst], ((kt + 1) / STAGES) & 1);
+        load_frags(a0, b0, nst, 0);
       }
+      mma_step(a1, b1);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }

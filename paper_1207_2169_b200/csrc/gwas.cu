@@ -253,8 +253,10 @@ gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw
 }
 
 // C[M x N] (row-major, ldc) = A[M x K] (rows K-contiguous, lda) * B[N x K]^T (rows K-contiguous, ldb)
+// group_m: rasterisation group along M (consecutive CTAs sweep group_m row tiles, then move along N): large for
+// K1 (the u8 X_R panels of a whole block stay in L2 while Z streams through once), small for K2.
 gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                    int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st) {
+                    int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st, int group_m = 16) {
   if (M <= 0 || N <= 0) return GWAS_OK;
   if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
   if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
@@ -271,7 +273,7 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.nsq = (int)std::min<int64_t>(nsq, N);
   s.tiles_m = (int)((M + kBM - 1) / kBM);
   s.tiles_n = (int)((N + kBN - 1) / kBN);
-  s.group_m = 16;
+  s.group_m = std::max(1, group_m);
   const bool sq = nsq < N;
   if (sq && (nsq % 32)) return fail(GWAS_E_ARG, "nsq must be a multiple of 32");
   if (a_u8) {
@@ -657,12 +659,12 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     }
     // K1 (Alg. 4 line 3): X_R'^T = X_R^T Z  (row i of xrp = Z^T g_i)
     CKG(c->tic(GWAS_K1, cs, &dummy));
-    CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs));
+    CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64));
     CKG(c->toc(cs));
     if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
     // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
     CKG(c->tic(GWAS_K2, cs, &dummy));
-    CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs));
+    CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs, 8));
     CKG(c->toc(cs));
     // K3 (Alg. 4 line 16): b_ij := S^-1 b_ij by Schur complement
     gw::SchurArgs a;

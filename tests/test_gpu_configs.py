@@ -1,0 +1,43 @@
+"""GPU parity at BASELINE.json's full sizes (configs 1-4), in the launch configuration bench.py times
+(uint8 X_R resident in HBM, k = 8192 blocks), checked on the seeded stratified subsample of reading A18
+(>= 10^4 pairs: <= 16 traits incl. 0 and t-1, SNPs incl. 0, m-1 and block edges) against the CPU oracle."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from gpu_helpers import TOL_B, TOL_VAR, compare
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4])
+def test_full_config_subsample(index):
+    import paper_1207_2169_b200 as gw
+    cfg = datagen.CONFIGS[index]
+    dev = torch.device("cuda", 0)
+    ds = datagen.dataset(cfg, device=dev)
+    ld = (cfg.n + 15) // 16 * 16
+    xr = torch.empty((cfg.m, ld), dtype=torch.uint8, pin_memory=True)
+    datagen.xr_dosages(cfg, ld=ld, out=xr.numpy())
+    xr_dev = xr.to(dev)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=8192)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    b, v, s = eng.run(xr_dev)
+    snps, traits = datagen.subsample(cfg)
+    idx_s = torch.from_numpy(snps).to(dev)
+    idx_t = torch.from_numpy(traits).to(dev)
+    bs = b.index_select(0, idx_s).index_select(1, idx_t).cpu().numpy()
+    vs = v.index_select(0, idx_s).index_select(1, idx_t).cpu().numpy()
+    ss = s.index_select(0, idx_s).index_select(1, idx_t).cpu().numpy()
+    assert int((s != 0).sum().item()) == int((s == 1).sum().item())  # no non-finite pairs anywhere
+    eng.close()
+    del xr_dev, b, v, s
+    G = datagen.xr_columns(cfg, snps)
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
+    eb, ev = compare(bs, vs, ss, ref)
+    print(f"C{index}: {snps.size} SNPs x {traits.size} traits = {snps.size * traits.size} pairs, "
+          f"max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
+    assert snps.size * traits.size >= 10_000
+    assert eb <= TOL_B and ev <= TOL_VAR
