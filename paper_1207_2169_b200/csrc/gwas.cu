@@ -664,7 +664,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
     // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
     CKG(c->tic(GWAS_K2, cs, &dummy));
-    CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs, 8));
+    CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs, 16));
     CKG(c->toc(cs));
     // K3 (Alg. 4 line 16): b_ij := S^-1 b_ij by Schur complement
     gw::SchurArgs a;
