@@ -200,7 +200,7 @@ def run_ours(args):
     datagen.xr_dosages(gcfg, lo, hi, ld=ld, out=xr_host.numpy())
     t_gen = time.perf_counter() - t0
 
-    eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True)
+    eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=args.int8_slices)
     setup = {}
     if rank == 0:
         eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
@@ -410,6 +410,8 @@ def main(argv=None):
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--block", type=int, default=8192, help="SNP columns per streamed block (k)")
     ap.add_argument("--snps", type=int, default=None, help="override m per rank (testing only)")
+    ap.add_argument("--int8-slices", type=int, default=0,
+                    help="0: K1/K2 on FP64 DMMA; 8: exact int8-sliced tcgen05 mode (NEXT-4)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--check", type=int, default=2000, help="oracle spot-check pairs after timing (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -73,7 +73,11 @@ typedef struct {
   void* compute_stream;    /* cudaStream_t for kernels (NULL = legacy default stream) */
   void* copy_stream;       /* cudaStream_t for host->HBM staging of X_R blocks (NULL = compute_stream) */
   int32_t timing;          /* 1 = bracket every K1/K2/K3/H2D launch with CUDA events (gwas_kernel_times) */
-  int32_t reserved;
+  int32_t int8_slices;     /* 0 (default): K1/K2 on the FP64 DMMA tensor pipe.  8: exact integer-sliced mode
+                              (requires xr_dtype = GWAS_XR_U8 and n <= 66000): X_R^T Z and
+                              the linear K2 terms X_R^T (Z D_j [X_L' | y'_j]) run as int8 tcgen05 products against
+                              8 signed digits of each fp64 column (exact int32 accumulation in TMEM), the
+                              W_R^T W_R term stays on DMMA.  Fixed at setup (part of the state). */
 } gwas_options;
 
 /* Fills the defaults listed above (device 0, u8 X_R). */

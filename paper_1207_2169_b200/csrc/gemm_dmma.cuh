@@ -51,12 +51,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Spin until the phase with the given parity has completed.  A bounded spin traps instead of hanging the
-// GPU if a pipeline bug ever loses an arrival (the trap surfaces as a launch failure on the host).
+// Spin until the phase with the given parity has completed.  A pipeline bug that loses an arrival traps after
+// ~10 s of waiting (checked on %globaltimer every 4096 tries) instead of hanging the GPU; the trap surfaces as a
+// launch failure on the host.  Legitimate waits are bounded by one tile's compute (milliseconds).
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
-  long long spins = 0;
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (true) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
@@ -64,7 +72,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(addr), "r"(parity)
         : "memory");
     if (done) return;
-    if (++spins > (1ll << 32)) __trap();
+    if ((++spins & 4095u) == 0) {
+      const uint64_t t = globaltimer_ns();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 10000000000ull) __trap();
+    }
   }
 }
 

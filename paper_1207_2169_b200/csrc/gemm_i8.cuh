@@ -1,0 +1,284 @@
+// K1i / K2a: exact integer-sliced products on the 5th-generation tensor cores (tcgen05.mma kind::i8, TMEM),
+// the "int8-sliced" mode of SURVEY.md §8(f) NEXT-4.
+//
+// X_R holds integer dosages (uint8, exact), so for any fp64 matrix B (columns b_c) the product X_R^T B can be
+// formed EXACTLY up to the representation of B: each column is scaled by a power of two 2^e_c with
+// |b_c| 2^-e_c <= 127/128 and split into S signed 8-bit digits (balanced, round-to-nearest):
+//       b_c 2^-e_c = sum_{s<S} d_s 2^{-7(s+1)} + r,   |d_0| <= 127, |d_{s>0}| <= 64, |r| <= 2^{-7S-1}
+// Every digit product sum_r g[r,i] d_s[r,c] is an exact int32 on the tensor core (|.| <= 255*127*n < 2^31 for
+// n <= 66 000), and the fp64 epilogue recombines the S int32 accumulators (Horner in 2^-7, one rounding per
+// digit) and applies 2^e_c.  With S = 8 the representation error is <= 2^-57 of the column maximum.
+//
+// Used for B = Z (Alg. 4 line 3: X_R' = Z^T X_R, needed for the W_R^T W_R term) and for the re-associated
+// linear terms of lines 13-15: W_R^T W_L = X_R^T (Z D_j X_L') and W_R^T Y_j = X_R^T (Z D_j y'_j),
+// i.e. B = B_lin = Z B_op (precomputed once in setup).  Both share the A operand, so one launch covers both:
+// output tiles [0, na_tiles) write C_a (X_R'^T), the rest write C_b (the linear block of the K2 output).
+//
+// Kernel: one 128 x 64 output tile per CTA.  B rows of a tile are stacked digit-major (row s*64 + j = digit s
+// of output column j), so the S*64 = 512 int32 accumulators of the tile fill TMEM exactly (512 columns x 128
+// lanes).  Warp 0: TMA producer (A box 64 B x 128 rows, B boxes 64 B x 256 rows, 64-byte swizzle) into a
+// STAGES ring; warp 1: TMEM allocation + single-thread tcgen05.mma issue (M = 128, N = 256, K = 32 per
+// instruction, two instructions per K step), tcgen05.commit -> mbarriers; warps 4-7: epilogue
+// (tcgen05.ld 32x32b, Horner recombination, fp64 stores).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gemm_dmma.cuh"  // smem_u32, mbarrier + TMA helpers
+
+namespace gw {
+
+constexpr int I8_SLICES = 8;       // digits per fp64 value
+constexpr int I8_NB = 64;          // output columns per tile
+constexpr int I8_BM = 128;         // output rows (SNPs) per tile
+constexpr int I8_BKB = 64;         // K bytes per stage (64-byte swizzle atom rows)
+constexpr int I8_STAGES = 5;
+constexpr int I8_THREADS = 256;
+constexpr int I8_BROWS = I8_SLICES * I8_NB;  // 512 B rows per tile = TMEM columns
+
+struct I8Shape {
+  int M;              // rows of A (SNPs of the block)
+  int K;              // n
+  int tiles_m, tiles_n;
+  int na_tiles;       // output tiles [0, na_tiles) -> C_a, the rest -> C_b
+  int na, nb;         // valid columns of C_a / C_b
+  double* Ca;
+  long long lda_c;
+  double* Cb;
+  long long ldb_c;
+  const int* exps;    // 2^e per output column of the concatenated digit matrix (tiles*64 entries)
+  int group_m;
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
+  // K-major, 64-byte swizzle: 8-row atoms of 64 B (SBO = 512 B between atoms), LBO unused (encoded 1),
+  // version 1 (sm_100), base offset 0 (tiles are 1024-byte aligned), layout type 4 = SWIZZLE_64B.
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
+// kind::i8 instruction descriptor: D s32, A u8, B s8, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(I8_THREADS, 1)
+    gemm_i8_sliced(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Shape s) {
+  constexpr int A_BYTES = I8_BM * I8_BKB;      // 8 KB
+  constexpr int B_BYTES = I8_BROWS * I8_BKB;   // 32 KB
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + I8_STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + I8_STAGES * B_BYTES);
+  uint64_t* empty = full + I8_STAGES;
+  uint64_t* tmem_full = empty + I8_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tm, tn;
+  {
+    const int pid = blockIdx.x;
+    const int per_group = s.group_m * s.tiles_n;
+    const int g = pid / per_group;
+    const int first_m = g * s.group_m;
+    const int gsz = min(s.tiles_m - first_m, s.group_m);
+    const int r = pid - g * per_group;
+    tm = first_m + r % gsz;
+    tn = r / gsz;
+  }
+  const int m0 = tm * I8_BM;
+  const int brow0 = tn * I8_BROWS;
+  const int KB = (s.K + I8_BKB - 1) / I8_BKB;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < I8_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {  // whole warp: allocate all 512 TMEM columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      for (int kb = 0; kb < KB; ++kb) {
+        const int st = kb % I8_STAGES;
+        if (kb >= I8_STAGES) mbar_wait(&empty[st], ((kb / I8_STAGES) - 1) & 1);
+        mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
+        tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * I8_BKB, m0);
+        tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * I8_BKB, brow0);
+        tma_load_2d(sB + st * B_BYTES + 256 * I8_BKB, &tmB, &full[st], kb * I8_BKB, brow0 + 256);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(256);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int st = kb % I8_STAGES;
+        mbar_wait(&full[st], (kb / I8_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + st * A_BYTES);
+        const uint32_t b0 = smem_u32(sB + st * B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < I8_BKB / 32; ++kk) {
+          const uint64_t ad = umma_desc_sw64(a0 + kk * 32);
+          const uint64_t bd0 = umma_desc_sw64(b0 + kk * 32);
+          const uint64_t bd1 = umma_desc_sw64(b0 + 256 * I8_BKB + kk * 32);
+          const uint32_t acc = (kb | kk) ? 1u : 0u;
+          umma_i8(tmem_base, ad, bd0, idesc, acc);
+          umma_i8(tmem_base + 256, ad, bd1, idesc, acc);
+        }
+        umma_commit(&empty[st]);  // frees the smem slot when these MMAs have read it
+      }
+      umma_commit(tmem_full);     // accumulators complete
+    }
+  } else if (warp >= 4) {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = tile rows
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int oc0 = tn * I8_NB;  // first output column of the concatenated digit matrix
+#pragma unroll 1
+    for (int j0 = 0; j0 < I8_NB; j0 += 16) {
+      double acc[16];
+      int32_t v[16];
+      tmem_ld16(tl + (I8_SLICES - 1) * I8_NB + j0, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc[c] = (double)v[c];
+#pragma unroll
+      for (int sl = I8_SLICES - 2; sl >= 0; --sl) {
+        tmem_ld16(tl + sl * I8_NB + j0, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[c] = fma(acc[c], 0.0078125, (double)v[c]);  // acc * 2^-7 + I_s
+      }
+      if (row < s.M) {
+        const bool in_a = tn < s.na_tiles;
+        double* crow = in_a ? s.Ca + (long long)row * s.lda_c : s.Cb + (long long)row * s.ldb_c;
+        const int cbase = in_a ? oc0 + j0 : (tn - s.na_tiles) * I8_NB + j0;
+        const int cmax = in_a ? s.na : s.nb;
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          const int e0 = __ldg(s.exps + oc0 + j0 + c), e1 = __ldg(s.exps + oc0 + j0 + c + 1);
+          const double x0 = scalbn(acc[c], e0 - 7), x1 = scalbn(acc[c + 1], e1 - 7);
+          const int col = cbase + c;
+          if (col + 1 < cmax) {
+            *reinterpret_cast<double2*>(crow + col) = make_double2(x0, x1);
+          } else if (col < cmax) {
+            crow[col] = x0;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// Setup helpers for the sliced mode.
+
+// Split rows of an fp64 matrix X (rows x ldx, K-contiguous, n valid entries) into S signed 8-bit digits.
+// Row `r` (an output column of the product) goes to digit rows dst_row(r, s) = (r / 64) * 512 + s * 64 + r % 64
+// of D (ldd bytes per row, pad zero); exps[r] = e with |X[r, :]| 2^-e <= 127/128.  One CTA per row.
+__global__ void digitize_rows(const double* __restrict__ X, long long ldx, int rows, int n, int row_off,
+                              int8_t* __restrict__ D, long long ldd, int* __restrict__ exps) {
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const double* x = X + (long long)r * ldx;
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) mx = fmax(mx, fabs(x[k]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  mx = red[0];
+  // smallest e with mx * 2^-e <= 127/128 (e = 0 for an all-zero row)
+  int e = 0;
+  if (mx > 0.0) {
+    frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+    if (ldexp(mx, -e) > 127.0 / 128.0) e += 1;
+  }
+  const int gr = r + row_off;
+  if (threadIdx.x == 0) exps[gr] = e;
+  const long long base = (long long)(gr / I8_NB) * I8_BROWS + gr % I8_NB;
+  for (int k = threadIdx.x; k < ldd; k += blockDim.x) {
+    double v = k < n ? ldexp(x[k], -e + 7) : 0.0;  // |v| <= 127
+#pragma unroll
+    for (int sl = 0; sl < I8_SLICES; ++sl) {
+      const double d = rint(v);
+      D[(base + (long long)sl * I8_NB) * ldd + k] = (int8_t)d;
+      v = (v - d) * 128.0;  // exact: |v - d| <= 1/2
+    }
+  }
+}
+
+// Out-of-place transpose of a kpad x kpad fp64 matrix (tiled through shared memory).
+__global__ void transpose_sq(const double* __restrict__ src, double* __restrict__ dst, int kpad) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = by + i, c = bx + threadIdx.x;
+    if (r < kpad && c < kpad) tile[i][threadIdx.x] = src[(long long)r * kpad + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = bx + i, c = by + threadIdx.x;
+    if (r < kpad && c < kpad) dst[(long long)r * kpad + c] = tile[threadIdx.x][i];
+  }
+}
+
+}  // namespace gw

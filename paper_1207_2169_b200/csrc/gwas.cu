@@ -16,6 +16,7 @@
 
 #include "../../include/gwas.h"
 #include "gemm_dmma.cuh"
+#include "gemm_i8.cuh"
 #include "schur.cuh"
 #include "setup_kernels.cuh"
 
@@ -66,6 +67,8 @@ struct StateHeader {
   int32_t output_mode, var_convention;
   double eps_collinear;
   int64_t off_Z, off_W, off_B2, off_Lpk, off_v, off_s2, off_betaT, off_dinv, total;
+  int32_t int8_slices, pad0;
+  int64_t na_pad, nlin, nlin_pad, off_dig, off_exps;  // int8-sliced mode: digit matrix of [Z | Z B_op] + 2^e
 };
 constexpr size_t kHeaderBytes = 512;
 static_assert(sizeof(StateHeader) <= kHeaderBytes, "header");
@@ -73,6 +76,8 @@ static_assert(sizeof(StateHeader) <= kHeaderBytes, "header");
 struct Dims {
   int64_t n, p, t, kpad, nsq, n2, ldc2, lds, kb;
   size_t es;
+  int i8;                          // int8-sliced mode
+  int64_t na_pad, nlin, nlin_pad;  // digit-matrix column blocks (multiples of 64)
 };
 
 Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
@@ -87,6 +92,10 @@ Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   d.lds = round_up(t * (p + 1), 2);
   d.kb = o->block_cols > 0 ? o->block_cols : 8192;
   d.es = o->xr_dtype == GWAS_XR_U8 ? 1 : 8;
+  d.i8 = o->int8_slices != 0;
+  d.na_pad = round_up(n, gw::I8_NB);
+  d.nlin = t * (p + 1);
+  d.nlin_pad = round_up(d.nlin, gw::I8_NB);
   return d;
 }
 
@@ -119,6 +128,14 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
   h.off_s2 = take(sizeof(double) * d.t);
   h.off_betaT = take(sizeof(double) * d.p * d.t);
   h.off_dinv = take(sizeof(double) * d.p * d.t);
+  h.int8_slices = o->int8_slices;
+  h.na_pad = d.na_pad;
+  h.nlin = d.nlin;
+  h.nlin_pad = d.nlin_pad;
+  if (d.i8) {
+    h.off_dig = take((size_t)((d.na_pad + d.nlin_pad) / gw::I8_NB) * gw::I8_BROWS * d.kpad);
+    h.off_exps = take(sizeof(int) * (d.na_pad + d.nlin_pad));
+  }
   h.total = (int64_t)off;
   return h;
 }
@@ -143,7 +160,7 @@ RunLayout run_layout(const Dims& d) {
 }
 
 struct SetupLayout {
-  size_t xlpad, ypad, xlp, yp, stl, h2, s2, err, info, work, total;
+  size_t xlpad, ypad, xlp, yp, stl, h2, s2, err, info, work, zt, blin, total;
 };
 SetupLayout setup_layout(const Dims& d, int64_t lwork) {
   SetupLayout s;
@@ -163,6 +180,11 @@ SetupLayout setup_layout(const Dims& d, int64_t lwork) {
   s.err = take(sizeof(unsigned long long) * 4);
   s.info = take(sizeof(int) * 4);
   s.work = take(sizeof(double) * (size_t)std::max<int64_t>(lwork, 1));
+  s.zt = s.blin = 0;
+  if (d.i8) {  // Z^T and B_lin = Z B_op (reuse the dsyevd workspace region's tail: allocated after it)
+    s.zt = take(sizeof(double) * d.kpad * d.kpad);
+    s.blin = take(sizeof(double) * d.nlin * d.kpad);
+  }
   s.total = off;
   return s;
 }
@@ -181,6 +203,12 @@ gwas_status check_sizes(int64_t n, int64_t p, int64_t t, const gwas_options* o) 
   if (!(o->eps_spd >= 0) || !(o->eps_collinear >= 0)) return fail(GWAS_E_ARG, "bad eps");
   const int64_t t_p2 = t * (p + 2) + 8;
   if (t_p2 > (1ll << 31) - 1) return fail(GWAS_E_ARG, "t too large");
+  if (o->int8_slices != 0) {
+    if (o->int8_slices != gw::I8_SLICES)
+      return fail(GWAS_E_ARG, "int8_slices = %d unsupported (0 or %d)", o->int8_slices, gw::I8_SLICES);
+    if (o->xr_dtype != GWAS_XR_U8) return fail(GWAS_E_ARG, "int8-sliced mode needs uint8 X_R (exact dosages)");
+    if (n > 66000) return fail(GWAS_E_ARG, "int8-sliced mode: n = %lld > 66000 (int32 accumulator bound)", (long long)n);
+  }
   return GWAS_OK;
 }
 
@@ -211,18 +239,20 @@ gwas_status get_encoder() {
 }
 
 // 2-D K-contiguous operand: rows x K elements, leading dimension ld (elements); box = 16 x box_rows.
-gwas_status make_map(CUtensorMap* map, const void* ptr, bool u8, int64_t K, int64_t rows, int64_t ld, int box_rows) {
+gwas_status make_map(CUtensorMap* map, const void* ptr, bool u8, int64_t K, int64_t rows, int64_t ld, int box_rows,
+                     int box_k = gw::GEMM_BK, int swizzle = -1) {
   CKG(get_encoder());
   const size_t es = u8 ? 1 : 8;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
-  cuuint32_t box[2] = {(cuuint32_t)gw::GEMM_BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_k, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * es) & 15))
     return fail(GWAS_E_ARG, "operand not 16-byte aligned (ptr %p, ld %lld)", ptr, (long long)ld);
   CUresult r = g_encode(map, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                         const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        u8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                        swizzle >= 0 ? (CUtensorMapSwizzle)swizzle
+                                     : (u8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B),
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(GWAS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return GWAS_OK;
@@ -302,6 +332,39 @@ gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
   return GWAS_OK;
 }
 
+// K1i/K2a: C_a[i][c] (c < na) and C_b[i][c'] (c' < nb) from the u8 A block and the stacked digit matrix.
+gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const int8_t* dig, int64_t ldd,
+                      int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
+                      double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st) {
+  if (M <= 0) return GWAS_OK;
+  CUtensorMap ma, mb;
+  CKG(make_map(&ma, A, true, K, M, lda, gw::I8_BM, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
+  CKG(make_map(&mb, dig, true, K, tiles_n * gw::I8_BROWS, ldd, 256, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
+  gw::I8Shape s;
+  s.M = (int)M;
+  s.K = (int)K;
+  s.tiles_m = (int)((M + gw::I8_BM - 1) / gw::I8_BM);
+  s.tiles_n = (int)tiles_n;
+  s.na_tiles = (int)na_tiles;
+  s.na = (int)na;
+  s.nb = (int)nb;
+  s.Ca = Ca;
+  s.lda_c = ldca;
+  s.Cb = Cb;
+  s.ldb_c = ldcb;
+  s.exps = exps;
+  s.group_m = 64;
+  constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  gw::gemm_i8_sliced<<<s.tiles_m * s.tiles_n, gw::I8_THREADS, smem, st>>>(ma, mb, s);
+  CKC(cudaGetLastError());
+  return GWAS_OK;
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -354,6 +417,8 @@ struct gwas_ctx {
   double* s2() const { return reinterpret_cast<double*>(state + h.off_s2); }
   double* betaT() const { return reinterpret_cast<double*>(state + h.off_betaT); }
   double* dinv() const { return reinterpret_cast<double*>(state + h.off_dinv); }
+  int8_t* dig() const { return reinterpret_cast<int8_t*>(state + h.off_dig); }
+  int* exps() const { return reinterpret_cast<int*>(state + h.off_exps); }
 
   cudaEvent_t ev() {
     if (!pool.empty()) {
@@ -551,6 +616,23 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
                                                                          o->eps_collinear, c->Lpk(), c->v(),
                                                                          c->betaT(), c->dinv(), derr + 1);
     CKC(cudaGetLastError());
+    if (d.i8) {
+      // sliced mode: B_lin = Z B_op (n x t(p+1), rows = output columns), then S-digit split of [Z | B_lin]
+      double* zt = reinterpret_cast<double*>(w + sl.zt);
+      double* blin = reinterpret_cast<double*>(w + sl.blin);
+      gw::transpose_sq<<<dim3((unsigned)((d.kpad + 31) / 32), (unsigned)((d.kpad + 31) / 32)), dim3(32, 8), 0, cs>>>(
+          c->Z(), zt, (int)d.kpad);
+      CKC(cudaGetLastError());
+      CKG(gemm_tn(false, c->B2(), d.kpad, zt, d.kpad, blin, d.kpad, d.nlin, n, n, n, cs));
+      const size_t dig_bytes = (size_t)((d.na_pad + d.nlin_pad) / gw::I8_NB) * gw::I8_BROWS * d.kpad;
+      CKC(cudaMemsetAsync(c->dig(), 0, dig_bytes, cs));
+      CKC(cudaMemsetAsync(c->exps(), 0, sizeof(int) * (d.na_pad + d.nlin_pad), cs));
+      gw::digitize_rows<<<(unsigned)n, 256, 0, cs>>>(c->Z(), d.kpad, (int)n, (int)n, 0, c->dig(), d.kpad, c->exps());
+      CKC(cudaGetLastError());
+      gw::digitize_rows<<<(unsigned)d.nlin, 256, 0, cs>>>(blin, d.kpad, (int)d.nlin, (int)n, (int)d.na_pad, c->dig(),
+                                                           d.kpad, c->exps());
+      CKC(cudaGetLastError());
+    }
     CKC(cudaEventRecord(e3, cs));
     unsigned long long herr[2];
     CKC(cudaMemcpyAsync(herr, derr, sizeof(herr), cudaMemcpyDeviceToHost, cs));
@@ -600,7 +682,8 @@ gwas_status gwas_attach(const gwas_options* o, int64_t n, int64_t p, int64_t t, 
   StateHeader got;
   CKC(cudaMemcpy(&got, state_dev, sizeof(got), cudaMemcpyDeviceToHost));
   if (got.magic != kMagic || got.version != kVersion || got.n != n || got.p != p || got.t != t ||
-      got.total != want.total || got.output_mode != o->output_mode || got.var_convention != o->var_convention)
+      got.total != want.total || got.output_mode != o->output_mode || got.var_convention != o->var_convention ||
+      got.int8_slices != o->int8_slices)
     return fail(GWAS_E_STATE, "state header does not match (n, p, t, options)");
   gwas_ctx* c = new gwas_ctx();
   gwas_status st = ctx_init(c, o, d, got, state_dev, work_dev, work_bytes);
@@ -657,15 +740,28 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       A = stage;
       lda = d.kpad;
     }
-    // K1 (Alg. 4 line 3): X_R'^T = X_R^T Z  (row i of xrp = Z^T g_i)
-    CKG(c->tic(GWAS_K1, cs, &dummy));
-    CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64));
-    CKG(c->toc(cs));
-    if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
-    // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
-    CKG(c->tic(GWAS_K2, cs, &dummy));
-    CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs, 16));
-    CKG(c->toc(cs));
+    if (!d.i8) {
+      // K1 (Alg. 4 line 3): X_R'^T = X_R^T Z  (row i of xrp = Z^T g_i)
+      CKG(c->tic(GWAS_K1, cs, &dummy));
+      CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64));
+      CKG(c->toc(cs));
+      if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
+      // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
+      CKG(c->tic(GWAS_K2, cs, &dummy));
+      CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs, 16));
+      CKG(c->toc(cs));
+    } else {
+      // K1i + K2a (int8-sliced, exact): X_R'^T = X_R^T Z and C[:, 0:t(p+1)] = X_R^T (Z B_op) in one launch
+      CKG(c->tic(GWAS_K1, cs, &dummy));
+      CKG(launch_i8(A, lda, cols, d.n, c->dig(), d.kpad, (d.na_pad + d.nlin_pad) / gw::I8_NB, d.na_pad / gw::I8_NB,
+                    c->exps(), xrp, d.kpad, d.n, c2, d.ldc2, d.nlin, cs));
+      CKG(c->toc(cs));
+      if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
+      // K2b (DMMA): C[:, nsq + j] = sum_k X_R'[k,i]^2 d_j[k]  (W_R^T W_R, the term that needs the rotation)
+      CKG(c->tic(GWAS_K2, cs, &dummy));
+      CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, 0, cs, 16));
+      CKG(c->toc(cs));
+    }
     // K3 (Alg. 4 line 16): b_ij := S^-1 b_ij by Schur complement
     gw::SchurArgs a;
     a.C = c2;

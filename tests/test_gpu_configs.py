@@ -12,8 +12,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("index", [1, 2, 3, 4])
-def test_full_config_subsample(index):
+@pytest.mark.parametrize("index,i8", [(1, 0), (2, 0), (3, 0), (4, 0), (1, 8), (2, 8), (3, 8), (4, 8)])
+def test_full_config_subsample(index, i8):
     import paper_1207_2169_b200 as gw
     cfg = datagen.CONFIGS[index]
     dev = torch.device("cuda", 0)
@@ -22,7 +22,7 @@ def test_full_config_subsample(index):
     xr = torch.empty((cfg.m, ld), dtype=torch.uint8, pin_memory=True)
     datagen.xr_dosages(cfg, ld=ld, out=xr.numpy())
     xr_dev = xr.to(dev)
-    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=8192)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=8192, int8_slices=i8)
     eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
     b, v, s = eng.run(xr_dev)
     snps, traits = datagen.subsample(cfg)
@@ -37,7 +37,7 @@ def test_full_config_subsample(index):
     G = datagen.xr_columns(cfg, snps)
     ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
     eb, ev = compare(bs, vs, ss, ref)
-    print(f"C{index}: {snps.size} SNPs x {traits.size} traits = {snps.size * traits.size} pairs, "
+    print(f"C{index} int8_slices={i8}: {snps.size} SNPs x {traits.size} traits = {snps.size * traits.size} pairs, "
           f"max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
     assert snps.size * traits.size >= 10_000
     assert eb <= TOL_B and ev <= TOL_VAR

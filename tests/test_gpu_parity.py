@@ -236,3 +236,48 @@ def test_attach_after_state_copy(c0):
     with pytest.raises(gw.GwasError) as e:
         wrong.attach()
     assert e.value.code in (6,)
+
+
+# ------------------------------------------------------------------ int8-sliced mode
+def test_int8_sliced_c0_all_pairs(c0):
+    cfg, ds, XR, ref = c0
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), int8_slices=8)
+    eb, ev = compare(b, v, s, ref)
+    print(f"C0 int8-sliced all pairs: max|db|/SE={eb:.3e} max Var rel={ev:.3e}")
+    assert eb <= TOL_B and ev <= TOL_VAR
+
+
+def test_int8_sliced_full_mode_and_invariance(c0):
+    cfg, ds, XR, ref = c0
+    dev = torch.from_numpy(XR).cuda()
+    b, v, s = _run(cfg, ds, dev, int8_slices=8, output_mode="full")
+    eb, ev = compare(b, v, s, ref, full=True)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+    base = _run(cfg, ds, dev, int8_slices=8)
+    for k in (333, 1):
+        other = _run(cfg, ds, dev[:300] if k == 1 else dev, int8_slices=8, block_cols=k)
+        for x, y in zip(base, other):
+            np.testing.assert_array_equal(x[: y.shape[0]], y)
+    other = _run(cfg, ds, torch.from_numpy(XR).pin_memory(), int8_slices=8, block_cols=700)
+    for x, y in zip(base, other):
+        np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("n,p,t,m,k", [(333, 3, 37, 777, 256), (17, 2, 1, 40, 16), (129, 6, 70, 300, 300),
+                                       (1000, 4, 200, 1000, 512)])
+def test_int8_sliced_ragged(n, p, t, m, k):
+    cfg = datagen.custom_config(n=n, p=p, m=m, t=t, index=400 + n)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), int8_slices=8, block_cols=k)
+    eb, ev = compare(b, v, s, ref)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+def test_int8_sliced_rejects_f64_dosages():
+    gw = _gw()
+    with pytest.raises(gw.GwasError):
+        gw.Gwas(64, 3, 2, device=0, xr_dtype="f64", int8_slices=8)
+    with pytest.raises(gw.GwasError):
+        gw.Gwas(64, 3, 2, device=0, int8_slices=5)
