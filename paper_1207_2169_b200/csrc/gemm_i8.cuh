@@ -82,6 +82,34 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Cluster helpers (TMA multicast of the digit slab across CTAs that share it).
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
@@ -90,6 +118,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+// CL = cluster size along M: the CL CTAs of a cluster compute CL consecutive row tiles of the same output
+// column tile, and each loads 1/CL of the shared digit slab and multicasts it to all (L2 reads of the dominant
+// B operand / CL).  Stage slots are released cluster-wide: every CTA's MMA completion arrives on every CTA's
+// empty barrier (count CL).
+template <int CL>
 __global__ void __launch_bounds__(I8_THREADS, 1)
     gemm_i8_sliced(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Shape s) {
   constexpr int A_BYTES = I8_BM * I8_BKB;      // 8 KB
@@ -105,14 +138,18 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tm, tn;
+  const uint32_t crank = CL > 1 ? cluster_ctarank() : 0u;
   {
-    const int pid = blockIdx.x;
-    const int per_group = s.group_m * s.tiles_n;
+    // grouped rasterisation over (row-tile clusters, column tiles); s.tiles_m is a multiple of CL
+    const int pid = blockIdx.x / CL;
+    const int tiles_mc = s.tiles_m / CL;
+    const int gm = max(1, s.group_m / CL);
+    const int per_group = gm * s.tiles_n;
     const int g = pid / per_group;
-    const int first_m = g * s.group_m;
-    const int gsz = min(s.tiles_m - first_m, s.group_m);
+    const int first_m = g * gm;
+    const int gsz = min(tiles_mc - first_m, gm);
     const int r = pid - g * per_group;
-    tm = first_m + r % gsz;
+    tm = (first_m + r % gsz) * CL + (int)crank;
     tn = r / gsz;
   }
   const int m0 = tm * I8_BM;
@@ -122,7 +159,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < I8_STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], CL);
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -134,6 +171,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
@@ -146,8 +184,14 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         if (kb >= I8_STAGES) mbar_wait(&empty[st], ((kb / I8_STAGES) - 1) & 1);
         mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
         tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * I8_BKB, m0);
-        tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * I8_BKB, brow0);
-        tma_load_2d(sB + st * B_BYTES + 256 * I8_BKB, &tmB, &full[st], kb * I8_BKB, brow0 + 256);
+        if constexpr (CL == 1) {
+          tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * I8_BKB, brow0);
+          tma_load_2d(sB + st * B_BYTES + 256 * I8_BKB, &tmB, &full[st], kb * I8_BKB, brow0 + 256);
+        } else {
+          constexpr int QR = I8_BROWS / CL;  // rows of the slab this CTA fetches for the whole cluster
+          tma_load_2d_mc(sB + st * B_BYTES + crank * QR * I8_BKB, &tmB, &full[st], kb * I8_BKB,
+                         brow0 + (int)crank * QR, (uint16_t)((1u << CL) - 1));
+        }
       }
     }
   } else if (warp == 1) {
@@ -168,7 +212,9 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
           umma_i8(tmem_base, ad, bd0, idesc, acc);
           umma_i8(tmem_base + 256, ad, bd1, idesc, acc);
         }
-        umma_commit(&empty[st]);  // frees the smem slot when these MMAs have read it
+        // frees the smem slot (in every CTA of the cluster) when these MMAs have read it
+        if constexpr (CL == 1) umma_commit(&empty[st]);
+        else umma_commit_mc(&empty[st], (uint16_t)((1u << CL) - 1));
       }
       umma_commit(tmem_full);     // accumulators complete
     }
@@ -216,6 +262,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(512));

@@ -337,13 +337,16 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
                       int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
                       double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st) {
   if (M <= 0) return GWAS_OK;
+  // cluster of 4 row tiles sharing each digit slab (multicast); small blocks use single CTAs
+  const int CL = (M >= 4 * gw::I8_BM) ? 4 : 1;
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, true, K, M, lda, gw::I8_BM, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
-  CKG(make_map(&mb, dig, true, K, tiles_n * gw::I8_BROWS, ldd, 256, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
+  CKG(make_map(&mb, dig, true, K, tiles_n * gw::I8_BROWS, ldd, CL == 1 ? 256 : gw::I8_BROWS / CL, gw::I8_BKB,
+               CU_TENSOR_MAP_SWIZZLE_64B));
   gw::I8Shape s;
   s.M = (int)M;
   s.K = (int)K;
-  s.tiles_m = (int)((M + gw::I8_BM - 1) / gw::I8_BM);
+  s.tiles_m = (int)round_up((M + gw::I8_BM - 1) / gw::I8_BM, CL);
   s.tiles_n = (int)tiles_n;
   s.na_tiles = (int)na_tiles;
   s.na = (int)na;
@@ -357,10 +360,28 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256;
   static bool attr_set = false;
   if (!attr_set) {
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  gw::gemm_i8_sliced<<<s.tiles_m * s.tiles_n, gw::I8_THREADS, smem, st>>>(ma, mb, s);
+  const unsigned grid = (unsigned)(s.tiles_m * s.tiles_n);
+  if (CL == 1) {
+    gw::gemm_i8_sliced<1><<<grid, gw::I8_THREADS, smem, st>>>(ma, mb, s);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(gw::I8_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4>, ma, mb, s));
+  }
   CKC(cudaGetLastError());
   return GWAS_OK;
 }

@@ -11,12 +11,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--cols", type=int, default=8192)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--int8-slices", type=int, default=0)
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.config]
 ld = (cfg.n + 15) // 16 * 16
 ds = datagen.dataset(cfg, device="cuda")
 XR = torch.from_numpy(datagen.xr_dosages(cfg, 0, a.cols, ld=ld)).cuda()
-eng = gw.Gwas(cfg.n, cfg.p, cfg.t, block_cols=a.cols, timing=True)
+eng = gw.Gwas(cfg.n, cfg.p, cfg.t, block_cols=a.cols, timing=True, int8_slices=a.int8_slices)
 eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
 out = eng.alloc_outputs(a.cols)
 for _ in range(a.reps):
