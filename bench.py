@@ -11,7 +11,10 @@ Setup (dsyevd, precompute, the one NCCL broadcast of the replicated state) is ti
 Scaling is weak: every rank processes its own m SNPs of the config (rank r takes SNP columns [r m, (r+1) m) of
 an N*m-SNP synthetic genome), so `value` = N*m*t / (max over ranks of the step time).
 
-`value`: X_R already resident in HBM (uint8 dosages, exact), timed with CUDA events on the compute stream.
+`value`: X_R already resident in HBM (uint8 dosages, exact), K1/K2 on the FP64 DMMA pipe (the north star's
+         design), blocks pipelined over two streams; timed with CUDA events on the compute stream.
+`roofline`: K1 from a serial pass of the same run (per-launch CUDA events; overlapped launches would share SMs).
+`modes.int8_sliced`: the exact int8-sliced tcgen05 mode on the same inputs.
 `e2e`:   the same through the public API from pinned HOST X_R (block staging on the copy stream inside the timed
          region) plus the device->host read of every step's b, Var and status.
 `--impl reference`: the CPU oracle (oracle/), as it stands, on a bounded sample of the same workload (rank 0).
@@ -171,6 +174,31 @@ def oracle_sample(cfg, ds, traits, snps):
 
 
 # ------------------------------------------------------------------ our arm
+def _timed_steps(eng, xr, out, steps, stream, barrier):
+    """`steps` full passes of the hot path between a barrier + synchronize on both sides; CUDA events on the
+    compute stream.  Returns ms."""
+    import torch
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        eng.run(xr, out=out)
+    e1.record(stream)
+    barrier()
+    return e0.elapsed_time(e1)
+
+
+def _kernel_pass(eng, xr, out, steps, barrier):
+    """Serial (non-overlapped) passes with per-launch CUDA events: the per-kernel durations behind `roofline`."""
+    eng.run(xr, out=out)
+    barrier()
+    eng.kernel_times(reset=True)
+    for _ in range(steps):
+        eng.run(xr, out=out)
+    barrier()
+    return eng.kernel_times(reset=True)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -200,52 +228,63 @@ def run_ours(args):
     datagen.xr_dosages(gcfg, lo, hi, ld=ld, out=xr_host.numpy())
     t_gen = time.perf_counter() - t0
 
-    eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=args.int8_slices)
-    setup = {}
-    if rank == 0:
-        eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
-        setup.update(eng.timings())
-    if world > 1:
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        replicate_state(eng.state, world)        # the one collective: replicated setup state over NVLink
-        e1.record()
-        torch.cuda.synchronize(dev)
-        setup["ms_broadcast"] = e0.elapsed_time(e1)
-        setup["broadcast_bytes"] = eng.state_bytes
-        if rank != 0:
-            eng.attach()
-
-    xr_dev = xr_host.to(dev)
-    out = eng.alloc_outputs(ncols)
-    stream = eng.compute_stream
-
     def barrier():
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
 
-    # ---------------- device-resident timed region (value)
+    def make_engine(i8, overlap):
+        """Rank 0 sets up (eig + precompute), the state is replicated by ONE broadcast, other ranks attach."""
+        eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=overlap)
+        info = {}
+        if rank == 0:
+            eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+            info.update(eng.timings())
+        if world > 1:
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            replicate_state(eng.state, world)   # the one collective: replicated setup state over NVLink
+            e1.record()
+            barrier()
+            info["ms_broadcast"] = e0.elapsed_time(e1)
+            info["broadcast_bytes"] = eng.state_bytes
+            if rank != 0:
+                eng.attach()
+        # a second, serial context on the same state (gwas_attach) times the kernels one by one
+        ser = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=False)
+        ser.state.copy_(eng.state)
+        ser.attach()
+        return eng, ser, info
+
+    xr_dev = xr_host.to(dev)
+    out = None
+    blocks = [min(args.block, ncols - c) for c in range(0, ncols, args.block)]
+    pairs_total = float(ncols) * t * world if args.scaling == "weak" else float(m_rank) * t
+    peak, peak_src = fp64_peak()
+    fl = [flops_per_block(n, p, t, c) for c in blocks]
+    k1_flops = sum(f["K1"] for f in fl)
+    k2_flops = sum(f["K2"] for f in fl)
+
+    # ================= headline mode: FP64 DMMA (the north star's K1/K2) =================
+    eng, ser, setup = make_engine(0, bool(args.overlap))
+    out = eng.alloc_outputs(ncols)
+    stream = eng.compute_stream
     for _ in range(args.warmup):
         eng.run(xr_dev, out=out)
-    barrier()
-    eng.kernel_times(reset=True)
     with ClockSampler(local) as clk:
-        barrier()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            eng.run(xr_dev, out=out)
-        ev1.record(stream)
-        barrier()
-    ms = ev0.elapsed_time(ev1)
-    kt = eng.kernel_times(reset=True)
+        ms = _timed_steps(eng, xr_dev, out, args.steps, stream, barrier)
     ms_max = max_over_ranks(ms, world, dev)
-    pairs_total = float(ncols) * t * world if args.scaling == "weak" else float(m_rank) * t
     value = pairs_total * args.steps / (ms_max / 1e3)
+    kt = _kernel_pass(ser, xr_dev, out, args.kernel_steps, barrier)
+    k1_ms, k2_ms, k3_ms = (kt[k]["ms"] / args.kernel_steps for k in ("K1", "K2", "K3"))
+    k1_tf = k1_flops / (k1_ms / 1e3) / 1e12
+    k2_tf = k2_flops / (k2_ms / 1e3) / 1e12
+    gemm_tf = (k1_flops + k2_flops) / ((k1_ms + k2_ms) / 1e3) / 1e12
+    k3_gbs = sum(k3_bytes(p, t, c) for c in blocks) / (k3_ms / 1e3) / 1e9
+    serial_ms = k1_ms + k2_ms + k3_ms
 
-    # ---------------- end-to-end through the public API from pinned host memory (e2e)
+    # e2e through the public API from pinned host memory (+ D2H of every step's results)
     b_h = torch.empty(out[0].shape, dtype=torch.float64, pin_memory=True)
     v_h = torch.empty(out[1].shape, dtype=torch.float64, pin_memory=True)
     s_h = torch.empty(out[2].shape, dtype=torch.int8, pin_memory=True)
@@ -260,70 +299,94 @@ def run_ours(args):
     e2e_steps = max(1, args.e2e_steps)
     e2e_step()
     barrier()
-    eng.kernel_times(reset=True)
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
         e2e_step()
     e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1), world, dev)
-    kt_e2e = eng.kernel_times(reset=True)
     e2e_value = pairs_total * e2e_steps / (ms_e2e / 1e3)
-    h2d = ncols * n * 1  # uint8 dosages actually copied (n of ld bytes per column... 1-D copy moves ld)
-    h2d = (ncols - 1) * ld + n
+    h2d = ((ncols - 1) * ld + n) if ncols else 0  # uint8 dosages copied per step
     d2h = b_h.numel() * 8 + v_h.numel() * 8 + s_h.numel()
+    res_fp64 = (b_h.numpy().copy(), v_h.numpy().copy(), s_h.numpy().copy()) if args.check and rank == 0 else None
+    eng.close()
+    ser.close()
+    del eng, ser
+
+    # ================= int8-sliced mode, same inputs =================
+    alt = None
+    if args.int8_alt:
+        eng8, ser8, setup8 = make_engine(8, True)
+        for _ in range(args.warmup):
+            eng8.run(xr_dev, out=out)
+        ms8 = max_over_ranks(_timed_steps(eng8, xr_dev, out, args.steps, eng8.compute_stream, barrier), world, dev)
+        value8 = pairs_total * args.steps / (ms8 / 1e3)
+        kt8 = _kernel_pass(ser8, xr_dev, out, args.kernel_steps, barrier)
+        i1_ms, i2_ms, i3_ms = (kt8[k]["ms"] / args.kernel_steps for k in ("K1", "K2", "K3"))
+        na_pad = (n + 63) // 64 * 64
+        nlin_pad = (t * (p + 1) + 63) // 64 * 64
+        i8_ops = sum(2.0 * c * (na_pad + nlin_pad) * 8 * n for c in blocks)   # int8 MACs x 2 actually issued
+        i8_peak = 2.0 * 1623.7  # MEASURED_PEAKS bf16 x the nominal int8/bf16 ratio (4.5 / 2.25)
+        k2b_flops = sum(2.0 * n * c * t for c in blocks)
+        alt = {"value": value8, "unit": UNIT, "ms_per_step": ms8 / args.steps,
+               "roofline": {"bound": "tensor", "kernel": "K1i+K2a int8-sliced tcgen05 (8 digits, TMEM int32)",
+                            "achieved": i8_ops / (i1_ms / 1e3) / 1e12, "peak": i8_peak, "unit": "TOPS",
+                            "frac": i8_ops / (i1_ms / 1e3) / 1e12 / i8_peak,
+                            "peak_source": "MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8/bf16 ratio)",
+                            "fp64_equiv_tflops": (k1_flops + sum(2.0 * n * c * t * (p + 1) for c in blocks))
+                                                 / (i1_ms / 1e3) / 1e12},
+               "k2b_dmma_tflops": k2b_flops / (i2_ms / 1e3) / 1e12,
+               "k2b_frac_of_fp64_peak": k2b_flops / (i2_ms / 1e3) / 1e12 / peak,
+               "share_of_serial_step": {k: v / (i1_ms + i2_ms + i3_ms) for k, v in
+                                        (("K1i+K2a", i1_ms), ("K2b", i2_ms), ("K3", i3_ms))},
+               "setup": setup8}
+        if args.check and rank == 0:
+            torch.cuda.synchronize(dev)
+            alt_res = (out[0].cpu().numpy(), out[1].cpu().numpy(), out[2].cpu().numpy())
+        eng8.close()
+        ser8.close()
 
     # ---------------- parity spot check on this run's outputs (outside timed regions)
     parity = None
     if args.check and rank == 0:
-        parity = spot_check(cfg, gcfg, ds, lo, hi, b_h.numpy(), v_h.numpy(), s_h.numpy(), args.check)
-
-    # ---------------- roofline of the dominant kernel (K1) and the GEMM stages
-    blocks = [min(args.block, ncols - c) for c in range(0, ncols, args.block)]
-    fl = [flops_per_block(n, p, t, c) for c in blocks]
-    k1_flops = sum(f["K1"] for f in fl) * args.steps
-    k2_flops = sum(f["K2"] for f in fl) * args.steps
-    peak, peak_src = fp64_peak()
-    k1_ms = kt["K1"]["ms"]
-    k2_ms = kt["K2"]["ms"]
-    k3_ms = kt["K3"]["ms"]
-    k1_tf = k1_flops / (k1_ms / 1e3) / 1e12
-    k2_tf = k2_flops / (k2_ms / 1e3) / 1e12
-    gemm_tf = (k1_flops + k2_flops) / ((k1_ms + k2_ms) / 1e3) / 1e12
-    k3_gbs = sum(k3_bytes(p, t, c) for c in blocks) * args.steps / (k3_ms / 1e3) / 1e9
-    traffic = ncu_traffic()
-    launches_per_step = 3 * len(blocks)
+        parity = spot_check(cfg, gcfg, ds, lo, hi, [res_fp64] + ([alt_res] if alt is not None else []), args.check)
+        if alt is not None:
+            alt["parity"] = parity.pop("extra")[0]
 
     res = None
     if rank == 0:
         clocks = clk.summary()
+        traffic = ncu_traffic()
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen, seeded)",
             "config": {"workload": f"{cfg.name}: n={n}, p={p}, m={m_rank}/rank, t={t}, k={args.block}, "
-                                   f"X_R uint8 dosages resident in HBM",
+                                   f"X_R uint8 dosages resident in HBM, K1/K2 FP64 DMMA",
                        "n": n, "p": p, "m_per_rank": ncols, "t": t, "block_cols": args.block,
                        "pairs_per_step": pairs_total, "parallelism": f"snp-shard x{world}",
+                       "overlap": bool(args.overlap),
                        "l2": "inputs larger than L2 (Z 0.8 GB, X_R 10 GB at C4); no flush"},
             "roofline": {"bound": "tensor", "kernel": "K1 rotation GEMM (FP64 DMMA)", "achieved": k1_tf,
                          "peak": peak, "unit": "TFLOP/s", "frac": k1_tf / peak,
                          "traffic": (traffic or {}).get("bytes_per_launch"),
                          "algorithmic_flops_per_launch": 2.0 * n * n * args.block,
-                         "avg_launch_ms": k1_ms / max(1, kt["K1"]["launches"]), "peak_source": peak_src},
+                         "avg_launch_ms": kt["K1"]["ms"] / max(1, kt["K1"]["launches"]),
+                         "timing": "CUDA events around every K1 launch, serial pass of the same run",
+                         "peak_source": peak_src},
             "gemm_stages": {"K1_tflops": k1_tf, "K2_tflops": k2_tf, "K1K2_tflops": gemm_tf,
                             "K1K2_frac_of_peak": gemm_tf / peak, "K3_hbm_gbs": k3_gbs,
-                            "share_of_step": {k: kt[k]["ms"] / ms for k in ("K1", "K2", "K3")}},
+                            "share_of_serial_step": {"K1": k1_ms / serial_ms, "K2": k2_ms / serial_ms,
+                                                     "K3": k3_ms / serial_ms}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": e2e_steps, "ms_per_step": ms_e2e / e2e_steps,
-                    "h2d_ms_per_step": kt_e2e["H2D"]["ms"] / e2e_steps},
-            "gpu_launches": launches_per_step * args.steps,
+                    "steps": e2e_steps, "ms_per_step": ms_e2e / e2e_steps},
+            "gpu_launches": 3 * len(blocks) * args.steps,
             "setup": {**setup, "datagen_s": t_gen},
             "clocks": clocks,
         }
+        if alt is not None:
+            res["modes"] = {"int8_sliced": alt}
         if parity is not None:
             res["parity"] = parity
         if not args.no_cpu_baseline:
@@ -332,7 +395,6 @@ def run_ours(args):
                                    "sample": f"{pairs} pairs of {cfg.name} ({args.cpu_traits} traits x "
                                              f"{args.cpu_snps} SNPs, Alg. 1 per problem, fp64 numpy/LAPACK), "
                                              f"{sec:.1f} s on {host_cores()} host cores"}
-    eng.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -346,8 +408,9 @@ def cpu_baseline_sample(cfg, ds, args):
     return oracle_sample(cfg, ds, traits, snps)
 
 
-def spot_check(cfg, gcfg, ds, lo, hi, b, v, s, npairs):
-    """Oracle on a seeded sample of this rank's pairs (after the timed regions)."""
+def spot_check(cfg, gcfg, ds, lo, hi, results, npairs):
+    """Oracle on a seeded sample of this rank's pairs (after the timed regions); `results` is a list of
+    (b, var, status) host arrays from different modes, all checked against the same oracle values."""
     import oracle
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from gpu_helpers import compare
@@ -358,9 +421,14 @@ def spot_check(cfg, gcfg, ds, lo, hi, b, v, s, npairs):
     loc = np.unique(np.concatenate([[0, hi - lo - 1], rng.choice(hi - lo, size=min(ns, hi - lo), replace=False)]))
     G = datagen.xr_columns(gcfg, loc + lo)
     ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
-    eb, ev = compare(b[np.ix_(loc, traits)], v[np.ix_(loc, traits)], s[np.ix_(loc, traits)], ref)
-    return {"pairs": int(loc.size * nt), "max_db_over_se": eb, "max_var_rel": ev, "tol": 1e-8,
-            "pass": bool(eb <= 1e-8 and ev <= 1e-8)}
+    outs = []
+    for b, v, s in results:
+        eb, ev = compare(b[np.ix_(loc, traits)], v[np.ix_(loc, traits)], s[np.ix_(loc, traits)], ref)
+        outs.append({"pairs": int(loc.size * nt), "max_db_over_se": eb, "max_var_rel": ev, "tol": 1e-8,
+                     "pass": bool(eb <= 1e-8 and ev <= 1e-8)})
+    res = dict(outs[0])
+    res["extra"] = outs[1:]
+    return res
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
@@ -410,8 +478,10 @@ def main(argv=None):
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--block", type=int, default=8192, help="SNP columns per streamed block (k)")
     ap.add_argument("--snps", type=int, default=None, help="override m per rank (testing only)")
-    ap.add_argument("--int8-slices", type=int, default=0,
-                    help="0: K1/K2 on FP64 DMMA; 8: exact int8-sliced tcgen05 mode (NEXT-4)")
+    ap.add_argument("--overlap", type=int, default=1, help="1: pipeline block b's K2/K3 beside block b+1's K1")
+    ap.add_argument("--kernel-steps", type=int, default=1, help="serial passes timed per kernel (roofline)")
+    ap.add_argument("--no-int8-alt", dest="int8_alt", action="store_false",
+                    help="skip the int8-sliced mode measurement reported under `modes`")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--check", type=int, default=2000, help="oracle spot-check pairs after timing (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

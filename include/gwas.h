@@ -78,6 +78,11 @@ typedef struct {
                               the linear K2 terms X_R^T (Z D_j [X_L' | y'_j]) run as int8 tcgen05 products against
                               8 signed digits of each fp64 column (exact int32 accumulation in TMEM), the
                               W_R^T W_R term stays on DMMA.  Fixed at setup (part of the state). */
+  int32_t overlap;         /* 1 = pipeline blocks over two streams: block b's K2 + K3 run on an internal auxiliary
+                              stream while block b+1's K1 runs on compute_stream (double-buffered intermediates;
+                              the library creates and owns that one stream).  gwas_run still completes on
+                              compute_stream.  Per-kernel event times then overlap.  Default 0. */
+  int32_t reserved;
 } gwas_options;
 
 /* Fills the defaults listed above (device 0, u8 X_R). */

@@ -26,7 +26,8 @@ class GwasOptions(C.Structure):
     _fields_ = [("device", C.c_int32), ("xr_dtype", C.c_int32), ("output_mode", C.c_int32),
                 ("var_convention", C.c_int32), ("block_cols", C.c_int64), ("eps_spd", C.c_double),
                 ("eps_collinear", C.c_double), ("compute_stream", C.c_void_p), ("copy_stream", C.c_void_p),
-                ("timing", C.c_int32), ("int8_slices", C.c_int32)]
+                ("timing", C.c_int32), ("int8_slices", C.c_int32),
+                ("overlap", C.c_int32), ("reserved", C.c_int32)]
 
 
 class GwasError(RuntimeError):

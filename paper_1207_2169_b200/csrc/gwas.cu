@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -141,9 +142,10 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
 }
 
 struct RunLayout {
-  size_t stage[2], xrp, c2, total;
+  size_t stage[2], xrp[2], c2[2], total;
 };
-RunLayout run_layout(const Dims& d) {
+// overlap mode double-buffers the rotated block and the K2 output so block b+1's K1 can run beside block b's K2/K3
+RunLayout run_layout(const Dims& d, bool overlap) {
   RunLayout r;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -153,8 +155,10 @@ RunLayout run_layout(const Dims& d) {
   };
   r.stage[0] = take(d.es * d.kpad * d.kb);
   r.stage[1] = take(d.es * d.kpad * d.kb);
-  r.xrp = take(sizeof(double) * d.kpad * d.kb);
-  r.c2 = take(sizeof(double) * d.ldc2 * d.kb);
+  r.xrp[0] = take(sizeof(double) * d.kpad * d.kb);
+  r.c2[0] = take(sizeof(double) * d.ldc2 * d.kb);
+  r.xrp[1] = overlap ? take(sizeof(double) * d.kpad * d.kb) : r.xrp[0];
+  r.c2[1] = overlap ? take(sizeof(double) * d.ldc2 * d.kb) : r.c2[0];
   r.total = off;
   return r;
 }
@@ -337,8 +341,15 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
                       int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
                       double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st) {
   if (M <= 0) return GWAS_OK;
-  // cluster of 4 row tiles sharing each digit slab (multicast); small blocks use single CTAs
-  const int CL = (M >= 4 * gw::I8_BM) ? 4 : 1;
+  // cluster of CL row tiles sharing each digit slab (multicast); small blocks use single CTAs.
+  // GWAS_I8_CLUSTER (1, 2 or 4) overrides the default of 2 (measured at C4: 1 -> 14.4 ms, 2 -> 8.8 ms,
+  // 4 -> 9.9 ms per 8192-column block; 4-CTA clusters leave SMs of some GPCs idle).
+  static int cl_env = [] {
+    const char* e = getenv("GWAS_I8_CLUSTER");
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  const int CL = (M >= (int64_t)cl_env * gw::I8_BM) ? cl_env : 1;
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, true, K, M, lda, gw::I8_BM, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
   CKG(make_map(&mb, dig, true, K, tiles_n * gw::I8_BROWS, ldd, CL == 1 ? 256 : gw::I8_BROWS / CL, gw::I8_BKB,
@@ -361,6 +372,7 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   static bool attr_set = false;
   if (!attr_set) {
     CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
@@ -375,12 +387,13 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4>, ma, mb, s));
+    if (CL == 2) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<2>, ma, mb, s));
+    else CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4>, ma, mb, s));
   }
   CKC(cudaGetLastError());
   return GWAS_OK;
@@ -416,7 +429,9 @@ struct gwas_ctx {
   size_t work_bytes = 0;
   RunLayout rl;
   cudaStream_t cs = nullptr, ps = nullptr;
+  cudaStream_t aux = nullptr;  // overlap mode: K2 + K3 of block b beside K1 of block b+1 (owned by the context)
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_k1[2] = {nullptr, nullptr}, ev_set_free[2] = {nullptr, nullptr}, ev_join = nullptr;
   int stage_next = 0;
   bool stage_zeroed = false;
   float ms_eig = 0.f, ms_pre = 0.f;
@@ -491,13 +506,17 @@ gwas_status ctx_init(gwas_ctx* c, const gwas_options* o, const Dims& d, const St
   c->state = static_cast<uint8_t*>(state);
   c->work = static_cast<uint8_t*>(work);
   c->work_bytes = work_bytes;
-  c->rl = run_layout(d);
+  c->rl = run_layout(d, o->overlap != 0);
   c->cs = static_cast<cudaStream_t>(o->compute_stream);
   c->ps = o->copy_stream ? static_cast<cudaStream_t>(o->copy_stream) : c->cs;
   for (int i = 0; i < 2; ++i) {
     CKC(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_k1[i], cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_set_free[i], cudaEventDisableTiming));
   }
+  CKC(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  if (o->overlap) CKC(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   return GWAS_OK;
 }
 
@@ -534,7 +553,7 @@ size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options*
   Dims d = make_dims(n, p, t, o);
   int64_t lwork = 0;
   if (dsyevd_lwork(o->device, n, d.kpad, &lwork) != GWAS_OK) return 0;
-  return std::max(setup_layout(d, lwork).total, run_layout(d).total);
+  return std::max(setup_layout(d, lwork).total, run_layout(d, o->overlap != 0).total);
 }
 
 gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, const double* phi, const double* XL,
@@ -551,7 +570,7 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
   int64_t lwork = 0;
   CKG(dsyevd_lwork(o->device, n, d.kpad, &lwork));
   SetupLayout sl = setup_layout(d, lwork);
-  RunLayout rl = run_layout(d);
+  RunLayout rl = run_layout(d, o->overlap != 0);
   if (state_bytes < (size_t)h.total) return fail(GWAS_E_NOMEM, "state %zu < %lld bytes", state_bytes, (long long)h.total);
   if (work_bytes < std::max(sl.total, rl.total))
     return fail(GWAS_E_NOMEM, "workspace %zu < %zu bytes", work_bytes, std::max(sl.total, rl.total));
@@ -698,7 +717,7 @@ gwas_status gwas_attach(const gwas_options* o, int64_t n, int64_t p, int64_t t, 
   Dims d = make_dims(n, p, t, o);
   StateHeader want = make_header(d, o);
   if (state_bytes < (size_t)want.total) return fail(GWAS_E_NOMEM, "state buffer too small");
-  RunLayout rl = run_layout(d);
+  RunLayout rl = run_layout(d, o->overlap != 0);
   if (work_bytes < rl.total) return fail(GWAS_E_NOMEM, "workspace %zu < %zu bytes", work_bytes, rl.total);
   StateHeader got;
   CKC(cudaMemcpy(&got, state_dev, sizeof(got), cudaMemcpyDeviceToHost));
@@ -733,11 +752,20 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
   const int64_t w = d.p + 1;
   const int64_t per_pair = c->opt.output_mode == GWAS_OUT_FULL ? w : 1;
   cudaStream_t cs = c->cs, ps = c->ps;
-  double* xrp = reinterpret_cast<double*>(c->work + c->rl.xrp);
-  double* c2 = reinterpret_cast<double*>(c->work + c->rl.c2);
+  const bool ovl = c->aux != nullptr;
+  cudaStream_t cs2 = ovl ? c->aux : cs;  // stream of K2 + K3
   cudaEvent_t dummy;
-  for (int64_t blk = 0; blk < ncols; blk += d.kb) {
+  if (ovl) {  // the aux stream starts after everything already enqueued on compute_stream
+    CKC(cudaEventRecord(c->ev_join, cs));
+    CKC(cudaStreamWaitEvent(cs2, c->ev_join, 0));
+  }
+  int64_t bi = 0;
+  for (int64_t blk = 0; blk < ncols; blk += d.kb, ++bi) {
     const int64_t cols = std::min<int64_t>(d.kb, ncols - blk);
+    const int set = ovl ? (int)(bi & 1) : 0;
+    double* xrp = reinterpret_cast<double*>(c->work + c->rl.xrp[set]);
+    double* c2 = reinterpret_cast<double*>(c->work + c->rl.c2[set]);
+    if (ovl) CKC(cudaStreamWaitEvent(cs, c->ev_set_free[set], 0));  // K2/K3 of block bi-2 done with this set
     const uint8_t* src = static_cast<const uint8_t*>(XR) + blk * ldx * (int64_t)d.es;
     const void* A = src;
     int64_t lda = ldx;
@@ -767,10 +795,14 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64));
       CKG(c->toc(cs));
       if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
+      if (ovl) {
+        CKC(cudaEventRecord(c->ev_k1[set], cs));
+        CKC(cudaStreamWaitEvent(cs2, c->ev_k1[set], 0));
+      }
       // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
-      CKG(c->tic(GWAS_K2, cs, &dummy));
-      CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs, 16));
-      CKG(c->toc(cs));
+      CKG(c->tic(GWAS_K2, cs2, &dummy));
+      CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, 16));
+      CKG(c->toc(cs2));
     } else {
       // K1i + K2a (int8-sliced, exact): X_R'^T = X_R^T Z and C[:, 0:t(p+1)] = X_R^T (Z B_op) in one launch
       CKG(c->tic(GWAS_K1, cs, &dummy));
@@ -778,10 +810,15 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
                     c->exps(), xrp, d.kpad, d.n, c2, d.ldc2, d.nlin, cs));
       CKG(c->toc(cs));
       if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
+      if (ovl) {
+        CKC(cudaEventRecord(c->ev_k1[set], cs));
+        CKC(cudaStreamWaitEvent(cs2, c->ev_k1[set], 0));
+      }
       // K2b (DMMA): C[:, nsq + j] = sum_k X_R'[k,i]^2 d_j[k]  (W_R^T W_R, the term that needs the rotation)
-      CKG(c->tic(GWAS_K2, cs, &dummy));
-      CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, 0, cs, 16));
-      CKG(c->toc(cs));
+      CKG(c->tic(GWAS_K2, cs2, &dummy));
+      CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, 0, cs2,
+                  16));
+      CKG(c->toc(cs2));
     }
     // K3 (Alg. 4 line 16): b_ij := S^-1 b_ij by Schur complement
     gw::SchurArgs a;
@@ -801,9 +838,14 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     a.b = b + blk * d.t * per_pair;
     a.var = var + blk * d.t * per_pair;
     a.status = status + blk * d.t;
-    CKG(c->tic(GWAS_K3, cs, &dummy));
-    CKG(launch_schur(a, (int)d.p, cs));
-    CKG(c->toc(cs));
+    CKG(c->tic(GWAS_K3, cs2, &dummy));
+    CKG(launch_schur(a, (int)d.p, cs2));
+    CKG(c->toc(cs2));
+    if (ovl) CKC(cudaEventRecord(c->ev_set_free[set], cs2));
+  }
+  if (ovl) {  // join: the call completes on compute_stream
+    CKC(cudaEventRecord(c->ev_join, cs2));
+    CKC(cudaStreamWaitEvent(cs, c->ev_join, 0));
   }
   return GWAS_OK;
 }
@@ -846,6 +888,13 @@ void gwas_destroy(gwas_ctx* c) {
   for (int i = 0; i < 2; ++i) {
     if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
     if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+    if (c->ev_k1[i]) cudaEventDestroy(c->ev_k1[i]);
+    if (c->ev_set_free[i]) cudaEventDestroy(c->ev_set_free[i]);
+  }
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
   }
   delete c;
 }

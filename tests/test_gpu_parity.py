@@ -107,6 +107,9 @@ def test_block_size_and_placement_invariance(c0):
         for x, y in zip(base, other):
             np.testing.assert_array_equal(x[: y.shape[0]], y)
     # pinned host input: 1-D staging copy (ld % 16 == 0) and 2-D staging copy (ld = n)
+    other = _run(cfg, ds, dev, block_cols=300, overlap=True)   # two-stream block pipelining
+    for x, y in zip(base, other):
+        np.testing.assert_array_equal(x, y)
     host_pad = torch.from_numpy(XR).pin_memory()
     host_n = torch.from_numpy(np.ascontiguousarray(XR[:, :cfg.n])).pin_memory()
     for src in (host_pad, host_n):
@@ -259,6 +262,9 @@ def test_int8_sliced_full_mode_and_invariance(c0):
         for x, y in zip(base, other):
             np.testing.assert_array_equal(x[: y.shape[0]], y)
     other = _run(cfg, ds, torch.from_numpy(XR).pin_memory(), int8_slices=8, block_cols=700)
+    for x, y in zip(base, other):
+        np.testing.assert_array_equal(x, y)
+    other = _run(cfg, ds, dev, int8_slices=8, block_cols=256, overlap=True)   # two-stream block pipelining
     for x, y in zip(base, other):
         np.testing.assert_array_equal(x, y)
 
