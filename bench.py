@@ -487,7 +487,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-traits", type=int, default=4)
     ap.add_argument("--cpu-snps", type=int, default=1024)
-    ap.add_argument("--ref-snps", type=int, default=64)
+    ap.add_argument("--ref-snps", type=int, default=1024)
     args = ap.parse_args(argv)
     rank, world, _ = dist_env()
     if world != args.gpus and rank == 0:

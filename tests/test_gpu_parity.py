@@ -287,3 +287,53 @@ def test_int8_sliced_rejects_f64_dosages():
         gw.Gwas(64, 3, 2, device=0, xr_dtype="f64", int8_slices=8)
     with pytest.raises(gw.GwasError):
         gw.Gwas(64, 3, 2, device=0, int8_slices=5)
+
+
+# ------------------------------------------------------------------ guard bands (compute-sanitizer is closed on this pool)
+@pytest.mark.parametrize("i8,ovl,mode", [(0, False, "snp"), (8, True, "full"), (0, True, "full"), (8, False, "snp")])
+def test_no_writes_outside_caller_buffers(i8, ovl, mode):
+    """Every buffer the library writes (state, workspace, b, var, status) sits between sentinel guard bands;
+    after setup + a ragged multi-block run from device and from pinned host memory the bands are intact."""
+    import ctypes as C
+    import paper_1207_2169_b200._lib as L
+    cfg = datagen.custom_config(n=333, p=3, m=700, t=37, index=501)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    o = L.default_options()
+    o.int8_slices, o.overlap, o.block_cols = i8, 1 if ovl else 0, 256
+    o.output_mode = L.OUT_FULL if mode == "full" else L.OUT_SNP
+    n, p, t, m = cfg.n, cfg.p, cfg.t, cfg.m
+    sb = L.lib.gwas_state_bytes(n, p, t, C.byref(o))
+    wb = L.lib.gwas_workspace_bytes(n, p, t, C.byref(o))
+    G = 1 << 16
+    per = (p + 1) if mode == "full" else 1
+
+    def guarded(nbytes):
+        buf = torch.full((nbytes + 2 * G,), 0xA5, dtype=torch.uint8, device="cuda")
+        return buf, buf[G:G + nbytes]
+
+    state_g, state = guarded(sb)
+    work_g, work = guarded(wb)
+    b_g, b = guarded(m * t * per * 8)
+    v_g, v = guarded(m * t * per * 8)
+    s_g, s = guarded(m * t)
+    ctx = C.c_void_p()
+    h2, s2 = np.ascontiguousarray(ds.h2), np.ascontiguousarray(ds.s2)
+    L.check(L.lib.gwas_setup(C.byref(o), n, p, t, ds.Phi.ctypes.data, np.asfortranarray(ds.XL).ctypes.data,
+                             np.asfortranarray(ds.Y).ctypes.data, h2.ctypes.data, s2.ctypes.data, state.data_ptr(), sb,
+                             work.data_ptr(), wb, C.byref(ctx)))
+    xd = torch.from_numpy(XR).cuda()
+    xh = torch.from_numpy(XR).pin_memory()
+    for src in (xd, xh):
+        L.check(L.lib.gwas_run(ctx, m, src.data_ptr(), XR.shape[1], b.data_ptr(), v.data_ptr(), s.data_ptr()))
+    torch.cuda.synchronize()
+    L.lib.gwas_destroy(ctx)
+    for g in (state_g, work_g, b_g, v_g, s_g):
+        assert bool((g[:G] == 0xA5).all()) and bool((g[-G:] == 0xA5).all())
+    # and the results are still right
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    bb = b.view(torch.float64).reshape(m, t, *((per,) if mode == "full" else ())).cpu().numpy()
+    vv = v.view(torch.float64).reshape(m, t, *((per,) if mode == "full" else ())).cpu().numpy()
+    ss = s.view(torch.int8).reshape(m, t).cpu().numpy()
+    eb, ev = compare(bb, vv, ss, ref, full=(mode == "full"))
+    assert eb <= TOL_B and ev <= TOL_VAR
