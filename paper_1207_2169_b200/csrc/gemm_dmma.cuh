@@ -134,10 +134,11 @@ __device__ __forceinline__ double load_a<double>(const uint8_t* a_tile, const do
 template <typename TA, int BM, int BN, int STAGES, bool SQ>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tn_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape s) {
-  constexpr int WARPS_N = 4;
+  constexpr int WARPS_N = BN / 32;  // warp tiles are always 32 columns wide (K2's squaring is per warp)
   constexpr int WARPS_M = GEMM_CONSUMER_WARPS / WARPS_N;
-  constexpr int WM = BM / WARPS_M;  // 64
+  constexpr int WM = BM / WARPS_M;  // 64 (BN = 128) or 32 (BN = 64)
   constexpr int WN = BN / WARPS_N;  // 32
+  static_assert(WN == 32 && WM % 8 == 0, "tile shape");
   constexpr int MI = WM / 8, NI = WN / 8;
   using L = GemmSmem<TA, BM, BN>;
 

@@ -262,20 +262,20 @@ gwas_status make_map(CUtensorMap* map, const void* ptr, bool u8, int64_t K, int6
   return GWAS_OK;
 }
 
-constexpr int kBM = 128, kBN = 128;
-constexpr int kStagesU8 = 8, kStagesF64 = 6;
+constexpr int kBM = 128;
+constexpr int kStagesU8 = 8, kStagesF64 = 6, kStagesF64N64 = 8;
 
-template <typename TA, int STAGES>
+template <typename TA, int BN, int STAGES>
 constexpr size_t gemm_smem_bytes() {
-  using L = gw::GemmSmem<TA, kBM, kBN>;
+  using L = gw::GemmSmem<TA, kBM, BN>;
   return 1024 + STAGES * (L::kAStride + L::kBStride) + 2 * STAGES * sizeof(uint64_t) + 256 * sizeof(double);
 }
 
-template <typename TA, int STAGES, bool SQ>
+template <typename TA, int BN, int STAGES, bool SQ>
 gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw::GemmShape& s, cudaStream_t st) {
   static bool attr_set = false;  // per instantiation (the library binds one device per process)
-  constexpr size_t smem = gemm_smem_bytes<TA, STAGES>();
-  auto kern = gw::gemm_tn_dmma<TA, kBM, kBN, STAGES, SQ>;
+  constexpr size_t smem = gemm_smem_bytes<TA, BN, STAGES>();
+  auto kern = gw::gemm_tn_dmma<TA, kBM, BN, STAGES, SQ>;
   if (!attr_set) {
     CKC(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
@@ -295,9 +295,13 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
   if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return fail(GWAS_E_ARG, "gemm dims too large");
+  // 128 x 64 tiles when 128 x 128 tiles would give fewer than 4 waves on 148 SMs (e.g. K2b, N = t):
+  // the wave tail dominates there, not the extra fragment loads of the narrower warp tiles
+  const int64_t tiles128 = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
+  const int bn = (tiles128 < 4 * 148 && N > 64) ? 64 : 128;
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, a_u8, K, M, lda, kBM));
-  CKG(make_map(&mb, B, false, K, N, ldb, kBN));
+  CKG(make_map(&mb, B, false, K, N, ldb, bn));
   gw::GemmShape s;
   s.M = (int)M;
   s.N = (int)N;
@@ -306,16 +310,24 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.ldc = ldc;
   s.nsq = (int)std::min<int64_t>(nsq, N);
   s.tiles_m = (int)((M + kBM - 1) / kBM);
-  s.tiles_n = (int)((N + kBN - 1) / kBN);
+  s.tiles_n = (int)((N + bn - 1) / bn);
   s.group_m = std::max(1, group_m);
   const bool sq = nsq < N;
   if (sq && (nsq % 32)) return fail(GWAS_E_ARG, "nsq must be a multiple of 32");
-  if (a_u8) {
-    if (sq) return launch_gemm_t<uint8_t, kStagesU8, true>(ma, mb, s, st);
-    return launch_gemm_t<uint8_t, kStagesU8, false>(ma, mb, s, st);
+  if (bn == 64) {
+    if (a_u8) {
+      if (sq) return launch_gemm_t<uint8_t, 64, kStagesU8, true>(ma, mb, s, st);
+      return launch_gemm_t<uint8_t, 64, kStagesU8, false>(ma, mb, s, st);
+    }
+    if (sq) return launch_gemm_t<double, 64, kStagesF64N64, true>(ma, mb, s, st);
+    return launch_gemm_t<double, 64, kStagesF64N64, false>(ma, mb, s, st);
   }
-  if (sq) return launch_gemm_t<double, kStagesF64, true>(ma, mb, s, st);
-  return launch_gemm_t<double, kStagesF64, false>(ma, mb, s, st);
+  if (a_u8) {
+    if (sq) return launch_gemm_t<uint8_t, 128, kStagesU8, true>(ma, mb, s, st);
+    return launch_gemm_t<uint8_t, 128, kStagesU8, false>(ma, mb, s, st);
+  }
+  if (sq) return launch_gemm_t<double, 128, kStagesF64, true>(ma, mb, s, st);
+  return launch_gemm_t<double, 128, kStagesF64, false>(ma, mb, s, st);
 }
 
 gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {

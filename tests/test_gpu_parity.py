@@ -49,7 +49,8 @@ def c0():
 # ------------------------------------------------------------------ K1/K2 kernel unit checks
 @pytest.mark.parametrize("M,N,K,u8,nsq", [(300, 200, 1000, True, None), (129, 131, 17, False, None),
                                           (1, 8, 16, False, None), (257, 300, 333, False, 160),
-                                          (8192, 136, 1000, True, None), (64, 500, 4096, False, 256)])
+                                          (8192, 136, 1000, True, None), (64, 500, 4096, False, 256),
+                                          (8192, 1500, 300, True, None), (8000, 1300, 99, False, 640)])
 def test_gemm_kernel_vs_fp64_reference(M, N, K, u8, nsq):
     gw = _gw()
     rng = np.random.default_rng(M * 7 + N)
