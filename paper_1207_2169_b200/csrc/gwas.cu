@@ -297,8 +297,13 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return fail(GWAS_E_ARG, "gemm dims too large");
   // 128 x 64 tiles when 128 x 128 tiles would give fewer than 4 waves on 148 SMs (e.g. K2b, N = t):
   // the wave tail dominates there, not the extra fragment loads of the narrower warp tiles
+  // GWAS_BN64_WAVES overrides the 4-wave threshold (0 = always 128 wide; tuning knob).
+  static int bn64_waves = [] {
+    const char* e = getenv("GWAS_BN64_WAVES");
+    return e ? atoi(e) : 4;
+  }();
   const int64_t tiles128 = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
-  const int bn = (tiles128 < 4 * 148 && N > 64) ? 64 : 128;
+  const int bn = (tiles128 < (int64_t)bn64_waves * 148 && N > 64) ? 64 : 128;
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, a_u8, K, M, lda, kBM));
   CKG(make_map(&mb, B, false, K, N, ldb, bn));

@@ -320,9 +320,9 @@ def test_no_writes_outside_caller_buffers(i8, ovl, mode):
     s_g, s = guarded(m * t)
     ctx = C.c_void_p()
     h2, s2 = np.ascontiguousarray(ds.h2), np.ascontiguousarray(ds.s2)
-    L.check(L.lib.gwas_setup(C.byref(o), n, p, t, ds.Phi.ctypes.data, np.asfortranarray(ds.XL).ctypes.data,
-                             np.asfortranarray(ds.Y).ctypes.data, h2.ctypes.data, s2.ctypes.data, state.data_ptr(), sb,
-                             work.data_ptr(), wb, C.byref(ctx)))
+    phi, xl, y = np.ascontiguousarray(ds.Phi), np.asfortranarray(ds.XL), np.asfortranarray(ds.Y)  # kept alive
+    L.check(L.lib.gwas_setup(C.byref(o), n, p, t, phi.ctypes.data, xl.ctypes.data, y.ctypes.data, h2.ctypes.data,
+                             s2.ctypes.data, state.data_ptr(), sb, work.data_ptr(), wb, C.byref(ctx)))
     xd = torch.from_numpy(XR).cuda()
     xh = torch.from_numpy(XR).pin_memory()
     for src in (xd, xh):
