@@ -118,6 +118,53 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+// Epilogue (warps 4-7): warp w drains TMEM lanes 32 (w % 4) .. +31 (= tile rows), recombines the S digit
+// accumulators of each output column (Horner in 2^-7, fp64), scales by 2^(e-7) and stores fp64.
+__device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base, uint64_t* tmem_full, int m0, int tn,
+                                            int warp, int lane) {
+  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = tile rows
+  const int q = warp & 3;
+  const int row = m0 + q * 32 + lane;
+  mbar_wait(tmem_full, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+  const int oc0 = tn * I8_NB;  // first output column of the concatenated digit matrix
+#pragma unroll 1
+  for (int j0 = 0; j0 < I8_NB; j0 += 16) {
+    double acc[16];
+    int32_t v[16];
+    tmem_ld16(tl + (I8_SLICES - 1) * I8_NB + j0, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = (double)v[c];
+#pragma unroll
+    for (int sl = I8_SLICES - 2; sl >= 0; --sl) {
+      tmem_ld16(tl + sl * I8_NB + j0, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc[c] = fma(acc[c], 0.0078125, (double)v[c]);  // acc * 2^-7 + I_s
+    }
+    if (row < s.M) {
+      const bool in_a = tn < s.na_tiles;
+      double* crow = in_a ? s.Ca + (long long)row * s.lda_c : s.Cb + (long long)row * s.ldb_c;
+      const int cbase = in_a ? oc0 + j0 : (tn - s.na_tiles) * I8_NB + j0;
+      const int cmax = in_a ? s.na : s.nb;
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) {
+        const int e0 = __ldg(s.exps + oc0 + j0 + c), e1 = __ldg(s.exps + oc0 + j0 + c + 1);
+        const double x0 = scalbn(acc[c], e0 - 7), x1 = scalbn(acc[c + 1], e1 - 7);
+        const int col = cbase + c;
+        if (col + 1 < cmax) {
+          *reinterpret_cast<double2*>(crow + col) = make_double2(x0, x1);
+        } else if (col < cmax) {
+          crow[col] = x0;
+        }
+      }
+    }
+  }
+
+}
+
 // CL = cluster size along M: the CL CTAs of a cluster compute CL consecutive row tiles of the same output
 // column tile, and each loads 1/CL of the shared digit slab and multicasts it to all (L2 reads of the dominant
 // B operand / CL).  Stage slots are released cluster-wide: every CTA's MMA completion arrives on every CTA's
@@ -219,46 +266,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       umma_commit(tmem_full);     // accumulators complete
     }
   } else if (warp >= 4) {
-    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = tile rows
-    const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
-    const int oc0 = tn * I8_NB;  // first output column of the concatenated digit matrix
-#pragma unroll 1
-    for (int j0 = 0; j0 < I8_NB; j0 += 16) {
-      double acc[16];
-      int32_t v[16];
-      tmem_ld16(tl + (I8_SLICES - 1) * I8_NB + j0, v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < 16; ++c) acc[c] = (double)v[c];
-#pragma unroll
-      for (int sl = I8_SLICES - 2; sl >= 0; --sl) {
-        tmem_ld16(tl + sl * I8_NB + j0, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-        for (int c = 0; c < 16; ++c) acc[c] = fma(acc[c], 0.0078125, (double)v[c]);  // acc * 2^-7 + I_s
-      }
-      if (row < s.M) {
-        const bool in_a = tn < s.na_tiles;
-        double* crow = in_a ? s.Ca + (long long)row * s.lda_c : s.Cb + (long long)row * s.ldb_c;
-        const int cbase = in_a ? oc0 + j0 : (tn - s.na_tiles) * I8_NB + j0;
-        const int cmax = in_a ? s.na : s.nb;
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          const int e0 = __ldg(s.exps + oc0 + j0 + c), e1 = __ldg(s.exps + oc0 + j0 + c + 1);
-          const double x0 = scalbn(acc[c], e0 - 7), x1 = scalbn(acc[c + 1], e1 - 7);
-          const int col = cbase + c;
-          if (col + 1 < cmax) {
-            *reinterpret_cast<double2*>(crow + col) = make_double2(x0, x1);
-          } else if (col < cmax) {
-            crow[col] = x0;
-          }
-        }
-      }
-    }
+    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -266,6 +274,146 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// 2-SM variant (tcgen05 cta_group::2): a CTA pair computes a 256 x 64 output tile with M = 256 MMAs issued by the
+// pair's leader CTA.  Each CTA stages its own 128 A rows and HALF of the 512-row digit slab (for each N = 256
+// chunk c, rows c*256 + rank*128 .. +127); the tensor cores of both SMs read both halves, so every slab byte is
+// fetched and written to shared memory once per pair (vs once per CTA), which relieves the shared-memory
+// bandwidth that bounds the 1-SM kernel (TMA writes + UMMA reads).  Each CTA's TMEM holds its own 128 rows x
+// 512 accumulator columns, drained by its own epilogue warps.  TMA loads of both CTAs signal the leader's full
+// barrier; the leader's commits arrive on both CTAs' empty / tmem_full barriers.
+constexpr int I8_STAGES2 = 8;
+
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  // the mbarrier operand addresses the LEADER CTA's barrier (peer bit cleared), as for 2-SM UMMA pipelines
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_leader)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_i8_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8_m256(int n) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(I8_THREADS, 1)
+    gemm_i8_sliced_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Shape s) {
+  constexpr int A_BYTES = I8_BM * I8_BKB;              // 8 KB: this CTA's 128 rows
+  constexpr int BH_BYTES = (I8_BROWS / 2) * I8_BKB;    // 16 KB: this CTA's half of the slab
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + I8_STAGES2 * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + I8_STAGES2 * BH_BYTES);
+  uint64_t* empty = full + I8_STAGES2;
+  uint64_t* tmem_full = empty + I8_STAGES2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  int tm, tn;
+  {
+    const int pid = blockIdx.x / 2;
+    const int tiles_mc = s.tiles_m / 2;
+    const int gm = max(1, s.group_m / 2);
+    const int per_group = gm * s.tiles_n;
+    const int g = pid / per_group;
+    const int first_m = g * gm;
+    const int gsz = min(tiles_mc - first_m, gm);
+    const int r = pid - g * per_group;
+    tm = (first_m + r % gsz) * 2 + (int)rank;
+    tn = r / gsz;
+  }
+  const int m0 = tm * I8_BM;
+  const int brow0 = tn * I8_BROWS;
+  const int KB = (s.K + I8_BKB - 1) / I8_BKB;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < I8_STAGES2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {  // both CTAs: one warp each, same smem slot
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      for (int kb = 0; kb < KB; ++kb) {
+        const int st = kb % I8_STAGES2;
+        if (kb >= I8_STAGES2) mbar_wait(&empty[st], ((kb / I8_STAGES2) - 1) & 1);
+        if (leader) mbar_expect_tx(&full[st], 2 * (A_BYTES + BH_BYTES));  // both CTAs' bytes land on it
+        tma_load_2d_2sm(sA + st * A_BYTES, &tmA, &full[st], kb * I8_BKB, m0);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d_2sm(sB + st * BH_BYTES + c * 128 * I8_BKB, &tmB, &full[st], kb * I8_BKB,
+                          brow0 + c * 256 + (int)rank * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_i8_m256(256);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int st = kb % I8_STAGES2;
+        mbar_wait(&full[st], (kb / I8_STAGES2) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + st * A_BYTES);
+        const uint32_t b0 = smem_u32(sB + st * BH_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < I8_BKB / 32; ++kk) {
+          const uint64_t ad = umma_desc_sw64(a0 + kk * 32);
+          const uint32_t acc = (kb | kk) ? 1u : 0u;
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            umma_i8_2sm(tmem_base + c * 256, ad, umma_desc_sw64(b0 + c * 128 * I8_BKB + kk * 32), idesc, acc);
+        }
+        umma_commit_2sm(&empty[st]);  // both CTAs may refill this stage once these MMAs have read it
+      }
+      umma_commit_2sm(tmem_full);
+    }
+  } else if (warp >= 4) {
+    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(512));
   }
 }
 

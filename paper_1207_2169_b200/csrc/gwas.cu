@@ -358,19 +358,24 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
                       int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
                       double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st) {
   if (M <= 0) return GWAS_OK;
-  // cluster of CL row tiles sharing each digit slab (multicast); small blocks use single CTAs.
-  // GWAS_I8_CLUSTER (1, 2 or 4) overrides the default of 2 (measured at C4: 1 -> 14.4 ms, 2 -> 8.8 ms,
-  // 4 -> 9.9 ms per 8192-column block; 4-CTA clusters leave SMs of some GPCs idle).
+  // GWAS_I8_KERNEL: "2sm" (default; CTA pairs with cta_group::2 MMAs), or "1sm" with GWAS_I8_CLUSTER (1, 2 or 4)
+  // CTAs multicasting the digit slab (tuning knobs; measured at C4 per 8192-column block: 1sm x1 14.4 ms,
+  // x2 8.8 ms, x4 9.9 ms).
+  static int mode_env = [] {
+    const char* e = getenv("GWAS_I8_KERNEL");
+    return (e && std::string(e) == "1sm") ? 1 : 2;
+  }();
   static int cl_env = [] {
     const char* e = getenv("GWAS_I8_CLUSTER");
     const int v = e ? atoi(e) : 2;
     return (v == 1 || v == 2 || v == 4) ? v : 2;
   }();
-  const int CL = (M >= (int64_t)cl_env * gw::I8_BM) ? cl_env : 1;
+  const bool two_sm = mode_env == 2 && M > gw::I8_BM;
+  const int CL = two_sm ? 2 : ((M >= (int64_t)cl_env * gw::I8_BM) ? cl_env : 1);
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, true, K, M, lda, gw::I8_BM, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
-  CKG(make_map(&mb, dig, true, K, tiles_n * gw::I8_BROWS, ldd, CL == 1 ? 256 : gw::I8_BROWS / CL, gw::I8_BKB,
-               CU_TENSOR_MAP_SWIZZLE_64B));
+  const int box_b = two_sm ? 128 : (CL == 1 ? 256 : gw::I8_BROWS / CL);
+  CKG(make_map(&mb, dig, true, K, tiles_n * gw::I8_BROWS, ldd, box_b, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
   gw::I8Shape s;
   s.M = (int)M;
   s.K = (int)K;
@@ -386,8 +391,10 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   s.exps = exps;
   s.group_m = 64;
   constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256;
+  constexpr size_t smem2 = 1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256;
   static bool attr_set = false;
   if (!attr_set) {
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -400,7 +407,7 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(gw::I8_THREADS);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = two_sm ? smem2 : smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -409,7 +416,8 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (CL == 2) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<2>, ma, mb, s));
+    if (two_sm) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced_2sm, ma, mb, s));
+    else if (CL == 2) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<2>, ma, mb, s));
     else CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4>, ma, mb, s));
   }
   CKC(cudaGetLastError());
