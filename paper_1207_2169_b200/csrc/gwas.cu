@@ -358,12 +358,12 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
                       int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
                       double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st) {
   if (M <= 0) return GWAS_OK;
-  // GWAS_I8_KERNEL: "2sm" (default; CTA pairs with cta_group::2 MMAs), or "1sm" with GWAS_I8_CLUSTER (1, 2 or 4)
-  // CTAs multicasting the digit slab (tuning knobs; measured at C4 per 8192-column block: 1sm x1 14.4 ms,
-  // x2 8.8 ms, x4 9.9 ms).
+  // GWAS_I8_KERNEL: "1sm" (default) with GWAS_I8_CLUSTER (1, 2 or 4; default 2) CTAs multicasting the digit
+  // slab, or "2sm" (CTA pairs with cta_group::2 MMAs).  Measured at C4 per 8192-column block: 1sm x1 14.4 ms,
+  // x2 8.8 ms, x4 9.9 ms; 2sm 9.4 ms.
   static int mode_env = [] {
     const char* e = getenv("GWAS_I8_KERNEL");
-    return (e && std::string(e) == "1sm") ? 1 : 2;
+    return (e && std::string(e) == "2sm") ? 2 : 1;
   }();
   static int cl_env = [] {
     const char* e = getenv("GWAS_I8_CLUSTER");

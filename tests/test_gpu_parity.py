@@ -338,3 +338,28 @@ def test_no_writes_outside_caller_buffers(i8, ovl, mode):
     ss = s.view(torch.int8).reshape(m, t).cpu().numpy()
     eb, ev = compare(bb, vv, ss, ref, full=(mode == "full"))
     assert eb <= TOL_B and ev <= TOL_VAR
+
+
+def test_int8_sliced_kernel_variants_agree(c0):
+    """The 1-SM (cluster 1, 2, 4) and 2-SM (cta_group::2) int8 kernels give bitwise identical results (the int32
+    digit products are exact, the fp64 recombination is the same code)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np, torch, datagen; sys.path.insert(0, 'tests');"
+            "import paper_1207_2169_b200 as gw;"
+            "cfg = datagen.custom_config(n=333, p=3, m=2000, t=37, index=601); ds = datagen.dataset(cfg);"
+            "X = torch.from_numpy(datagen.xr_dosages(cfg, ld=336)).cuda();"
+            "e = gw.Gwas(cfg.n, cfg.p, cfg.t, int8_slices=8, block_cols=1024); e.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2);"
+            "b, v, s = e.run(X); torch.cuda.synchronize();"
+            "np.save(sys.argv[1], np.stack([b.cpu().numpy(), v.cpu().numpy()]))")
+    outs = []
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        for i, (kern, cl) in enumerate((("1sm", "1"), ("1sm", "2"), ("1sm", "4"), ("2sm", "2"))):
+            f = os.path.join(d, f"r{i}.npy")
+            env = dict(os.environ, GWAS_I8_KERNEL=kern, GWAS_I8_CLUSTER=cl)
+            subprocess.run([sys.executable, "-c", code, f], check=True, env=env, cwd=os.path.dirname(os.path.dirname(__file__)))
+            outs.append(np.load(f))
+    for o in outs[1:]:
+        np.testing.assert_array_equal(outs[0], o)
