@@ -338,11 +338,15 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
 gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
   const long long np = (long long)a.cols * a.t;
   if (np == 0) return GWAS_OK;
-  const int threads = 256;
-  const unsigned grid = (unsigned)((np + threads - 1) / threads);
+  const int threads = 128;
+  gw::SchurArgs args = a;
+  args.tj = 1;
+  while (args.tj < a.t && args.tj < threads) args.tj *= 2;
+  const int snps_per_block = (threads / args.tj) * gw::SCHUR_ICH;
+  const dim3 grid((unsigned)((a.t + args.tj - 1) / args.tj), (unsigned)((a.cols + snps_per_block - 1) / snps_per_block));
   switch (p) {
 #define CASE_P(P) \
-  case P: gw::schur_solve<P><<<grid, threads, 0, st>>>(a); break;
+  case P: gw::schur_solve<P><<<grid, threads, 0, st>>>(args); break;
     CASE_P(1) CASE_P(2) CASE_P(3) CASE_P(4) CASE_P(5) CASE_P(6)
     CASE_P(7) CASE_P(8) CASE_P(9) CASE_P(10) CASE_P(11) CASE_P(12)
 #undef CASE_P

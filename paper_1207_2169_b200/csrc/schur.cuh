@@ -10,8 +10,7 @@
 //        b_g = (r - u.v_j) / sigma,  Var_gg = 1 / sigma                        (textbook Var, reading A1)
 //   full output mode adds q = L_j^-T u,  b_L = S_TL_j^-1 b_T_j - q b_g,  diag Var_L = diag(S_TL_j^-1) + q^2/sigma.
 // Collinear SNP (reading A6): sigma <= eps * c -> status 1, NaN payload; non-finite -> status 2.
-// One thread per pair, trait index fastest, so a warp reads 32 consecutive traits of one C row (coalesced)
-// and writes 32 consecutive outputs.  HBM-bound: 8(p+2) bytes in, 17 (SNP mode) bytes out per pair.
+// HBM-bound: 8(p+2) bytes in, 17 (SNP mode) bytes out per pair.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -31,76 +30,91 @@ struct SchurArgs {
   double eps_collinear;
   int literal;        // var_convention 1: Var *= sigma2_j
   int full;           // output mode
+  int tj;             // threads per block along traits (power of two <= 128); the rest of the block spans SNPs
   double* b;
   double* var;
   int8_t* status;
 };
 
+constexpr int SCHUR_ICH = 16;  // SNPs per thread: the trait's factors are loaded once per 16 pairs
+
+// One thread per (trait j, chunk of SCHUR_ICH SNPs); with t >= 32 a warp covers 32 consecutive traits, so the C
+// reads and the output writes are coalesced, and the per-trait L_TL_j, v_j stay in registers across the chunk.
 template <int P>
-__global__ void __launch_bounds__(256) schur_solve(SchurArgs s) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long npairs = (long long)s.cols * s.t;
-  if (idx >= npairs) return;
-  const int i = (int)(idx / s.t);
-  const int j = (int)(idx - (long long)i * s.t);
+__global__ void __launch_bounds__(128) schur_solve(SchurArgs s) {
+  const int j = blockIdx.x * s.tj + (int)(threadIdx.x % (unsigned)s.tj);
+  const int ii = (int)(threadIdx.x / (unsigned)s.tj);
+  if (j >= s.t) return;
   const int t = s.t;
-  const double* row = s.C + (long long)i * s.ldc;
-
-  double u[P];
-  double uv = 0.0, uu = 0.0;
+  double L[P * (P + 1) / 2], Linv_d[P], v[P];
+#pragma unroll
+  for (int e = 0; e < P * (P + 1) / 2; ++e) L[e] = __ldg(s.Lpk + (long long)e * t + j);
 #pragma unroll
   for (int f = 0; f < P; ++f) {
-    double acc = __ldg(row + f * t + j);
-#pragma unroll
-    for (int l = 0; l < f; ++l) acc -= __ldg(s.Lpk + (long long)(f * (f + 1) / 2 + l) * t + j) * u[l];
-    u[f] = acc / __ldg(s.Lpk + (long long)(f * (f + 1) / 2 + f) * t + j);
-    uu += u[f] * u[f];
-    uv += u[f] * __ldg(s.v + (long long)f * t + j);
+    Linv_d[f] = 1.0 / L[f * (f + 1) / 2 + f];
+    v[f] = __ldg(s.v + (long long)f * t + j);
   }
-  const double r = __ldg(row + P * t + j);
-  const double c = __ldg(row + s.nsq + j);
-  const double sigma = c - uu;
   const double scale = s.literal ? __ldg(s.s2 + j) : 1.0;
-
-  int8_t st = 0;
-  if (!(isfinite(sigma) && isfinite(c) && isfinite(r) && isfinite(uv))) st = 2;
-  else if (!(sigma > s.eps_collinear * c)) st = 1;
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
-  double bg = nan, vg = nan;
-  if (st == 0) {
-    bg = (r - uv) / sigma;
-    vg = scale / sigma;
-    if (!(isfinite(bg) && isfinite(vg))) { st = 2; bg = vg = nan; }
-  }
-  s.status[idx] = st;
-  if (!s.full) {
-    s.b[idx] = bg;
-    s.var[idx] = vg;
-    return;
-  }
-  // full mode: q = L^-T u (back substitution), then the X_L coefficients
-  double q[P];
+  const int i0 = (blockIdx.y * (blockDim.x / s.tj) + ii) * SCHUR_ICH;
+  const int i1 = min(s.cols, i0 + SCHUR_ICH);
+  for (int i = i0; i < i1; ++i) {
+    const double* row = s.C + (long long)i * s.ldc;
+    const long long idx = (long long)i * t + j;
+    double u[P];
+    double uv = 0.0, uu = 0.0;
 #pragma unroll
-  for (int f = P - 1; f >= 0; --f) {
-    double acc = u[f];
+    for (int f = 0; f < P; ++f) {
+      double acc = __ldg(row + f * t + j);
 #pragma unroll
-    for (int l = f + 1; l < P; ++l) acc -= __ldg(s.Lpk + (long long)(l * (l + 1) / 2 + f) * t + j) * q[l];
-    q[f] = acc / __ldg(s.Lpk + (long long)(f * (f + 1) / 2 + f) * t + j);
-  }
-  double* bo = s.b + idx * (P + 1);
-  double* vo = s.var + idx * (P + 1);
-#pragma unroll
-  for (int f = 0; f < P; ++f) {
-    if (st == 0) {
-      bo[f] = __ldg(s.betaT + (long long)f * t + j) - q[f] * bg;
-      vo[f] = scale * (__ldg(s.dinv + (long long)f * t + j) + q[f] * q[f] / sigma);
-    } else {
-      bo[f] = nan;
-      vo[f] = nan;
+      for (int l = 0; l < f; ++l) acc -= L[f * (f + 1) / 2 + l] * u[l];
+      u[f] = acc * Linv_d[f];
+      uu += u[f] * u[f];
+      uv += u[f] * v[f];
     }
+    const double r = __ldg(row + P * t + j);
+    const double c = __ldg(row + s.nsq + j);
+    const double sigma = c - uu;
+    int8_t st = 0;
+    if (!(isfinite(sigma) && isfinite(c) && isfinite(r) && isfinite(uv))) st = 2;
+    else if (!(sigma > s.eps_collinear * c)) st = 1;
+    double bg = nan, vg = nan;
+    if (st == 0) {
+      const double rs = 1.0 / sigma;
+      bg = (r - uv) * rs;
+      vg = scale * rs;
+      if (!(isfinite(bg) && isfinite(vg))) { st = 2; bg = vg = nan; }
+    }
+    s.status[idx] = st;
+    if (!s.full) {
+      s.b[idx] = bg;
+      s.var[idx] = vg;
+      continue;
+    }
+    // full mode: q = L^-T u (back substitution), then the X_L coefficients
+    double q[P];
+#pragma unroll
+    for (int f = P - 1; f >= 0; --f) {
+      double acc = u[f];
+#pragma unroll
+      for (int l = f + 1; l < P; ++l) acc -= L[l * (l + 1) / 2 + f] * q[l];
+      q[f] = acc * Linv_d[f];
+    }
+    double* bo = s.b + idx * (P + 1);
+    double* vo = s.var + idx * (P + 1);
+#pragma unroll
+    for (int f = 0; f < P; ++f) {
+      if (st == 0) {
+        bo[f] = __ldg(s.betaT + (long long)f * t + j) - q[f] * bg;
+        vo[f] = scale * (__ldg(s.dinv + (long long)f * t + j) + q[f] * q[f] / sigma);
+      } else {
+        bo[f] = nan;
+        vo[f] = nan;
+      }
+    }
+    bo[P] = bg;
+    vo[P] = vg;
   }
-  bo[P] = bg;
-  vo[P] = vg;
 }
 
 }  // namespace gw
