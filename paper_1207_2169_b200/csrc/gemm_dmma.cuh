@@ -32,7 +32,21 @@ struct GemmShape {
   int nsq;        // first column using A∘A (>= N: none)
   int tiles_m, tiles_n;
   int group_m;    // rasterisation group along M (L2 reuse of B panels)
+  int ksplit;     // K split into ksplit ranges of kt_per_split 16-wide k-tiles (skinny N); partial products of
+  int kt_per_split;  // split s go to C + s * split_stride (summed in fixed order by splitk_reduce)
+  long long split_stride;
 };
+
+// Fixed-order sum of the split-K partial products: C[i][c] = sum_s P_s[i][c] (deterministic, independent of M).
+__global__ void splitk_reduce(const double* __restrict__ P, long long split_stride, int ksplit, int M, int N,
+                              long long ldp, double* __restrict__ C, long long ldc) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)M * N) return;
+  const int i = (int)(idx / N), c = (int)(idx - (long long)i * N);
+  double acc = P[(long long)i * ldp + c];
+  for (int sp = 1; sp < ksplit; ++sp) acc += P[sp * split_stride + (long long)i * ldp + c];
+  C[(long long)i * ldc + c] = acc;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -156,8 +170,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   // grouped rasterisation: consecutive CTAs walk down a group of group_m row tiles, then move along N
   int tm, tn;
+  const int split = blockIdx.x % s.ksplit;
   {
-    const int pid = blockIdx.x;
+    const int pid = blockIdx.x / s.ksplit;
     const int per_group = s.group_m * s.tiles_n;
     const int g = pid / per_group;
     const int first_m = g * s.group_m;
@@ -167,7 +182,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tn = r / gsz;
   }
   const int m0 = tm * BM, n0 = tn * BN;
-  const int KT = (s.K + GEMM_BK - 1) / GEMM_BK;
+  const int kt_begin = split * s.kt_per_split;
+  const int KT = min((s.K + GEMM_BK - 1) / GEMM_BK - kt_begin, s.kt_per_split);  // k-tiles of this CTA (>= 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -188,8 +204,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int st = kf % STAGES;
     if (kf >= STAGES) mbar_wait(&empty[st], ((kf / STAGES) - 1) & 1);
     mbar_expect_tx(&full[st], L::kATile + L::kBTile);
-    tma_load_2d(sA + st * L::kAStride, &tmA, &full[st], kf * GEMM_BK, m0);
-    tma_load_2d(sB + st * L::kBStride, &tmB, &full[st], kf * GEMM_BK, n0);
+    tma_load_2d(sA + st * L::kAStride, &tmA, &full[st], (kt_begin + kf) * GEMM_BK, m0);
+    tma_load_2d(sB + st * L::kBStride, &tmB, &full[st], (kt_begin + kf) * GEMM_BK, n0);
   };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -288,7 +304,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   for (int i = 0; i < MI; ++i) {
     const int row = m0 + wm * WM + i * 8 + g;
     if (row >= s.M) continue;
-    double* crow = s.C + (long long)row * s.ldc;
+    double* crow = s.C + split * s.split_stride + (long long)row * s.ldc;
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
       const int col = n0 + wn * WN + j * 8 + 2 * q;

@@ -142,7 +142,7 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
 }
 
 struct RunLayout {
-  size_t stage[2], xrp[2], c2[2], total;
+  size_t stage[2], xrp[2], c2[2], split[2], total;
 };
 // overlap mode double-buffers the rotated block and the K2 output so block b+1's K1 can run beside block b's K2/K3
 RunLayout run_layout(const Dims& d, bool overlap) {
@@ -159,6 +159,8 @@ RunLayout run_layout(const Dims& d, bool overlap) {
   r.c2[0] = take(sizeof(double) * d.ldc2 * d.kb);
   r.xrp[1] = overlap ? take(sizeof(double) * d.kpad * d.kb) : r.xrp[0];
   r.c2[1] = overlap ? take(sizeof(double) * d.ldc2 * d.kb) : r.c2[0];
+  r.split[0] = take(sizeof(double) * 8 * 64 * d.kb);  // split-K partials of skinny K2 products (kSplitMax x kSplitLd)
+  r.split[1] = overlap ? take(sizeof(double) * 8 * 64 * d.kb) : r.split[0];
   r.total = off;
   return r;
 }
@@ -280,7 +282,7 @@ gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw
     CKC(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  const int grid = s.tiles_m * s.tiles_n;
+  const int grid = s.tiles_m * s.tiles_n * s.ksplit;
   kern<<<grid, gw::GEMM_THREADS, smem, st>>>(ma, mb, s);
   CKC(cudaGetLastError());
   return GWAS_OK;
@@ -289,8 +291,13 @@ gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw
 // C[M x N] (row-major, ldc) = A[M x K] (rows K-contiguous, lda) * B[N x K]^T (rows K-contiguous, ldb)
 // group_m: rasterisation group along M (consecutive CTAs sweep group_m row tiles, then move along N): large for
 // K1 (the u8 X_R panels of a whole block stay in L2 while Z streams through once), small for K2.
+// split_scratch (optional, >= kSplitMax * M * kSplitLd doubles): skinny products (N <= 64, one column tile, K >= 4096)
+// are split along K into fixed ranges (independent of M, so results stay bitwise invariant to the block size)
+// and summed in fixed order.
+constexpr int kSplitMax = 8, kSplitLd = 64;
 gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                    int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st, int group_m = 16) {
+                    int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st, int group_m = 16,
+                    double* split_scratch = nullptr) {
   if (M <= 0 || N <= 0) return GWAS_OK;
   if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
   if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
@@ -303,7 +310,7 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
     return e ? atoi(e) : 4;
   }();
   const int64_t tiles128 = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
-  const int bn = (tiles128 < (int64_t)bn64_waves * 148 && N > 64) ? 64 : 128;
+  const int bn = (N <= 64 || tiles128 < (int64_t)bn64_waves * 148) ? 64 : 128;
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, a_u8, K, M, lda, kBM));
   CKG(make_map(&mb, B, false, K, N, ldb, bn));
@@ -317,22 +324,45 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.tiles_m = (int)((M + kBM - 1) / kBM);
   s.tiles_n = (int)((N + bn - 1) / bn);
   s.group_m = std::max(1, group_m);
+  const int kt_all = (int)((K + gw::GEMM_BK - 1) / gw::GEMM_BK);
+  s.ksplit = 1;
+  s.kt_per_split = kt_all;
+  s.split_stride = 0;
+  double* c_final = C;
+  int64_t ldc_final = ldc;
+  if (split_scratch && N <= kSplitLd && kt_all >= 256) {
+    s.kt_per_split = (kt_all + kSplitMax - 1) / kSplitMax;
+    s.ksplit = (kt_all + s.kt_per_split - 1) / s.kt_per_split;
+    s.C = split_scratch;
+    s.ldc = kSplitLd;
+    s.split_stride = (long long)M * kSplitLd;
+  }
   const bool sq = nsq < N;
   if (sq && (nsq % 32)) return fail(GWAS_E_ARG, "nsq must be a multiple of 32");
-  if (bn == 64) {
-    if (a_u8) {
-      if (sq) return launch_gemm_t<uint8_t, 64, kStagesU8, true>(ma, mb, s, st);
-      return launch_gemm_t<uint8_t, 64, kStagesU8, false>(ma, mb, s, st);
+  auto launch = [&]() -> gwas_status {
+    if (bn == 64) {
+      if (a_u8) {
+        if (sq) return launch_gemm_t<uint8_t, 64, kStagesU8, true>(ma, mb, s, st);
+        return launch_gemm_t<uint8_t, 64, kStagesU8, false>(ma, mb, s, st);
+      }
+      if (sq) return launch_gemm_t<double, 64, kStagesF64N64, true>(ma, mb, s, st);
+      return launch_gemm_t<double, 64, kStagesF64N64, false>(ma, mb, s, st);
     }
-    if (sq) return launch_gemm_t<double, 64, kStagesF64N64, true>(ma, mb, s, st);
-    return launch_gemm_t<double, 64, kStagesF64N64, false>(ma, mb, s, st);
+    if (a_u8) {
+      if (sq) return launch_gemm_t<uint8_t, 128, kStagesU8, true>(ma, mb, s, st);
+      return launch_gemm_t<uint8_t, 128, kStagesU8, false>(ma, mb, s, st);
+    }
+    if (sq) return launch_gemm_t<double, 128, kStagesF64, true>(ma, mb, s, st);
+    return launch_gemm_t<double, 128, kStagesF64, false>(ma, mb, s, st);
+  };
+  CKG(launch());
+  if (s.ksplit > 1) {
+    const long long total = M * N;
+    gw::splitk_reduce<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s.C, s.split_stride, s.ksplit, (int)M, (int)N,
+                                                                       kSplitLd, c_final, ldc_final);
+    CKC(cudaGetLastError());
   }
-  if (a_u8) {
-    if (sq) return launch_gemm_t<uint8_t, 128, kStagesU8, true>(ma, mb, s, st);
-    return launch_gemm_t<uint8_t, 128, kStagesU8, false>(ma, mb, s, st);
-  }
-  if (sq) return launch_gemm_t<double, 128, kStagesF64, true>(ma, mb, s, st);
-  return launch_gemm_t<double, 128, kStagesF64, false>(ma, mb, s, st);
+  return GWAS_OK;
 }
 
 gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
@@ -794,6 +824,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     const int set = ovl ? (int)(bi & 1) : 0;
     double* xrp = reinterpret_cast<double*>(c->work + c->rl.xrp[set]);
     double* c2 = reinterpret_cast<double*>(c->work + c->rl.c2[set]);
+    double* splitbuf = reinterpret_cast<double*>(c->work + c->rl.split[set]);
     if (ovl) CKC(cudaStreamWaitEvent(cs, c->ev_set_free[set], 0));  // K2/K3 of block bi-2 done with this set
     const uint8_t* src = static_cast<const uint8_t*>(XR) + blk * ldx * (int64_t)d.es;
     const void* A = src;
@@ -830,7 +861,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       }
       // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
       CKG(c->tic(GWAS_K2, cs2, &dummy));
-      CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, 16));
+      CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, 16, splitbuf));
       CKG(c->toc(cs2));
     } else {
       // K1i + K2a (int8-sliced, exact): X_R'^T = X_R^T Z and C[:, 0:t(p+1)] = X_R^T (Z B_op) in one launch
@@ -846,7 +877,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       // K2b (DMMA): C[:, nsq + j] = sum_k X_R'[k,i]^2 d_j[k]  (W_R^T W_R, the term that needs the rotation)
       CKG(c->tic(GWAS_K2, cs2, &dummy));
       CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, 0, cs2,
-                  16));
+                  16, splitbuf));
       CKG(c->toc(cs2));
     }
     // K3 (Alg. 4 line 16): b_ij := S^-1 b_ij by Schur complement

@@ -363,3 +363,18 @@ def test_int8_sliced_kernel_variants_agree(c0):
             outs.append(np.load(f))
     for o in outs[1:]:
         np.testing.assert_array_equal(outs[0], o)
+
+
+@pytest.mark.parametrize("i8", [0, 8])
+def test_split_k_skinny_products(i8):
+    """n >= 4096 with few traits: the skinny K2 / K2b products are split along K (fixed ranges, fixed-order sum)."""
+    cfg = datagen.custom_config(n=4100, p=2, m=300, t=3, index=700)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), int8_slices=i8, block_cols=128)
+    eb, ev = compare(b, v, s, ref)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+    b2, v2, s2 = _run(cfg, ds, torch.from_numpy(XR).cuda(), int8_slices=i8, block_cols=300, overlap=True)
+    np.testing.assert_array_equal(b, b2)
+    np.testing.assert_array_equal(v, v2)
