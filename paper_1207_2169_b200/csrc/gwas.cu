@@ -291,7 +291,7 @@ gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw
 // C[M x N] (row-major, ldc) = A[M x K] (rows K-contiguous, lda) * B[N x K]^T (rows K-contiguous, ldb)
 // group_m: rasterisation group along M (consecutive CTAs sweep group_m row tiles, then move along N): large for
 // K1 (the u8 X_R panels of a whole block stay in L2 while Z streams through once), small for K2.
-// split_scratch (optional, >= kSplitMax * M * kSplitLd doubles): skinny products (N <= 64, one column tile, K >= 4096)
+// split_scratch (optional, >= kSplitMax * M * kSplitLd doubles): skinny products (N <= 64, one column tile, K >= 256)
 // are split along K into fixed ranges (independent of M, so results stay bitwise invariant to the block size)
 // and summed in fixed order.
 constexpr int kSplitMax = 8, kSplitLd = 64;
@@ -330,8 +330,8 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.split_stride = 0;
   double* c_final = C;
   int64_t ldc_final = ldc;
-  if (split_scratch && N <= kSplitLd && kt_all >= 256) {
-    s.kt_per_split = (kt_all + kSplitMax - 1) / kSplitMax;
+  if (split_scratch && N <= kSplitLd && kt_all >= 16) {
+    s.kt_per_split = std::max(8, (kt_all + kSplitMax - 1) / kSplitMax);
     s.ksplit = (kt_all + s.kt_per_split - 1) / s.kt_per_split;
     s.C = split_scratch;
     s.ldc = kSplitLd;
@@ -372,7 +372,8 @@ gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
   gw::SchurArgs args = a;
   args.tj = 1;
   while (args.tj < a.t && args.tj < threads) args.tj *= 2;
-  const int snps_per_block = (threads / args.tj) * gw::SCHUR_ICH;
+  args.ich = a.t >= 32 ? gw::SCHUR_ICH : 1;
+  const int snps_per_block = (threads / args.tj) * args.ich;
   const dim3 grid((unsigned)((a.t + args.tj - 1) / args.tj), (unsigned)((a.cols + snps_per_block - 1) / snps_per_block));
   switch (p) {
 #define CASE_P(P) \

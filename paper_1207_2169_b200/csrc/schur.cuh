@@ -31,6 +31,7 @@ struct SchurArgs {
   int literal;        // var_convention 1: Var *= sigma2_j
   int full;           // output mode
   int tj;             // threads per block along traits (power of two <= 128); the rest of the block spans SNPs
+  int ich;            // SNPs per thread (SCHUR_ICH when t >= 32; 1 for few traits, so a warp reads consecutive rows)
   double* b;
   double* var;
   int8_t* status;
@@ -56,8 +57,8 @@ __global__ void __launch_bounds__(128) schur_solve(SchurArgs s) {
   }
   const double scale = s.literal ? __ldg(s.s2 + j) : 1.0;
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
-  const int i0 = (blockIdx.y * (blockDim.x / s.tj) + ii) * SCHUR_ICH;
-  const int i1 = min(s.cols, i0 + SCHUR_ICH);
+  const int i0 = (blockIdx.y * (blockDim.x / s.tj) + ii) * s.ich;
+  const int i1 = min(s.cols, i0 + s.ich);
   for (int i = i0; i < i1; ++i) {
     const double* row = s.C + (long long)i * s.ldc;
     const long long idx = (long long)i * t + j;
