@@ -50,7 +50,7 @@ typedef enum {
                           non-finite inputs, unaligned ld, unpinned host X_R, ... */
   GWAS_E_NOT_SPD = 2,  /* some sigma2_j (h2_j w_k + 1 - h2_j) <= eps_spd (reading A7), or S_TL_j not SPD
                           (X_L rank-deficient); message names j (and k) */
-  GWAS_E_EIG = 3,      /* cusolverDnDsyevd reported info != 0 */
+  GWAS_E_EIG = 3,      /* cusolverDnDsyevd (or, for GWAS_ALG_CHOL, dtrtri) reported info != 0 */
   GWAS_E_CUDA = 4,     /* a CUDA / cuSOLVER runtime error */
   GWAS_E_NOMEM = 5,    /* caller-provided state or workspace smaller than gwas_state_bytes / _workspace_bytes */
   GWAS_E_STATE = 6     /* wrong call order, or a state buffer whose header does not match (gwas_attach) */
@@ -61,6 +61,7 @@ enum { GWAS_OUT_SNP = 0, GWAS_OUT_FULL = 1 };      /* outputs per pair: (b_g, Va
 enum { GWAS_VAR_TEXTBOOK = 0, GWAS_VAR_LITERAL = 1 };
 enum { GWAS_PAIR_OK = 0, GWAS_PAIR_COLLINEAR = 1, GWAS_PAIR_NONFINITE = 2 };
 enum { GWAS_K1 = 0, GWAS_K2 = 1, GWAS_K3 = 2, GWAS_H2D = 3, GWAS_NUM_TIMERS = 4 };
+enum { GWAS_ALG_EIG = 0, GWAS_ALG_CHOL = 1 };
 
 typedef struct {
   int32_t device;          /* CUDA ordinal the context binds to */
@@ -82,7 +83,11 @@ typedef struct {
                               stream while block b+1's K1 runs on compute_stream (double-buffered intermediates;
                               the library creates and owns that one stream).  gwas_run still completes on
                               compute_stream.  Per-kernel event times then overlap.  Default 0. */
-  int32_t reserved;
+  int32_t algorithm;       /* GWAS_ALG_EIG (default): CLAK-Eig, Alg. 4, any t.
+                              GWAS_ALG_CHOL: CLAK-Chol single-trait analysis, Alg. 3, t == 1 only:
+                              M = sigma2 (h2 Phi + (1 - h2) I) = L L^T (cuSOLVER dpotrf) and L^-1 (dtrtri) replace
+                              the eigendecomposition; K1 becomes X_R := L^-1 X_R on the lower triangle only
+                              (half the flops of Z^T X_R), K2/K3 run with D = I.  Fixed at setup (state). */
 } gwas_options;
 
 /* Fills the defaults listed above (device 0, u8 X_R). */
@@ -97,7 +102,7 @@ GWAS_API size_t gwas_state_bytes(int64_t n, int64_t p, int64_t t, const gwas_opt
  * the rotated block X_R' + the block's reductions).  Queries cuSOLVER on opt->device.  0 on error. */
 GWAS_API size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* opt);
 
-/* Alg. 4 lines 1-2, 4, 6-11.
+/* Alg. 4 lines 1-2, 4, 6-11; with GWAS_ALG_CHOL, Alg. 3 lines 1-3, 5-7.
  *   phi    n x n symmetric (col-major, ld = n), host or device, read-only
  *   XL     n x p (col-major, ld = n), column 0 is the intercept (any full-column-rank X_L is accepted)
  *   Y      n x t (col-major, ld = n)

@@ -15,6 +15,7 @@ OUT_SNP, OUT_FULL = 0, 1
 VAR_TEXTBOOK, VAR_LITERAL = 0, 1
 PAIR_OK, PAIR_COLLINEAR, PAIR_NONFINITE = 0, 1, 2
 K1, K2, K3, H2D = 0, 1, 2, 3
+ALG_EIG, ALG_CHOL = 0, 1
 NUM_TIMERS = 4
 
 EXPORTS = ["gwas_default_options", "gwas_state_bytes", "gwas_workspace_bytes", "gwas_setup", "gwas_attach",
@@ -27,7 +28,7 @@ class GwasOptions(C.Structure):
                 ("var_convention", C.c_int32), ("block_cols", C.c_int64), ("eps_spd", C.c_double),
                 ("eps_collinear", C.c_double), ("compute_stream", C.c_void_p), ("copy_stream", C.c_void_p),
                 ("timing", C.c_int32), ("int8_slices", C.c_int32),
-                ("overlap", C.c_int32), ("reserved", C.c_int32)]
+                ("overlap", C.c_int32), ("algorithm", C.c_int32)]
 
 
 class GwasError(RuntimeError):

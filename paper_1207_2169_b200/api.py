@@ -21,6 +21,7 @@ from ._lib import check, lib
 _XR = {"u8": _lib.XR_U8, "f64": _lib.XR_F64}
 _OUT = {"snp": _lib.OUT_SNP, "full": _lib.OUT_FULL}
 _VAR = {"textbook": _lib.VAR_TEXTBOOK, "literal": _lib.VAR_LITERAL}
+_ALG = {"eig": _lib.ALG_EIG, "chol": _lib.ALG_CHOL}
 
 
 def _ptr(x) -> int:
@@ -45,7 +46,7 @@ class Gwas:
     def __init__(self, n: int, p: int, t: int, *, device: int = 0, xr_dtype: str = "u8", output_mode: str = "snp",
                  var_convention: str = "textbook", block_cols: int = 8192, timing: bool = False,
                  eps_spd: float = 1e-10, eps_collinear: float = 1e-10, compute_stream=None, copy_stream=None,
-                 int8_slices: int = 0, overlap: bool = False):
+                 int8_slices: int = 0, overlap: bool = False, algorithm: str = "eig"):
         self.n, self.p, self.t = int(n), int(p), int(t)
         self.w = self.p + 1
         self.device = torch.device("cuda", device)
@@ -66,6 +67,7 @@ class Gwas:
         o.timing = 1 if timing else 0
         o.int8_slices = int(int8_slices)
         o.overlap = 1 if overlap else 0
+        o.algorithm = _ALG[algorithm]
         self.opt = o
         self.state_bytes = lib.gwas_state_bytes(self.n, self.p, self.t, C.byref(o))
         if self.state_bytes == 0:

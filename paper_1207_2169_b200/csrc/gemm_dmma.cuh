@@ -35,6 +35,8 @@ struct GemmShape {
   int ksplit;     // K split into ksplit ranges of kt_per_split 16-wide k-tiles (skinny N); partial products of
   int kt_per_split;  // split s go to C + s * split_stride (summed in fixed order by splitk_reduce)
   long long split_stride;
+  int tri;        // B lower-triangular in (row, k): row c has no entries at k > c (CLAK-Chol's L^-1), so an output
+                  // tile [n0, n0 + BN) only needs k < n0 + BN
 };
 
 // Fixed-order sum of the split-K partial products: C[i][c] = sum_s P_s[i][c] (deterministic, independent of M).
@@ -183,7 +185,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   const int m0 = tm * BM, n0 = tn * BN;
   const int kt_begin = split * s.kt_per_split;
-  const int KT = min((s.K + GEMM_BK - 1) / GEMM_BK - kt_begin, s.kt_per_split);  // k-tiles of this CTA (>= 1)
+  const int k_end = s.tri ? min(s.K, n0 + BN) : s.K;
+  const int KT = min((k_end + GEMM_BK - 1) / GEMM_BK - kt_begin, s.kt_per_split);  // k-tiles of this CTA (>= 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {

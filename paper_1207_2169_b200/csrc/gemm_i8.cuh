@@ -49,6 +49,7 @@ struct I8Shape {
   long long ldb_c;
   const int* exps;    // 2^e per output column of the concatenated digit matrix (tiles*64 entries)
   int group_m;
+  int tri_tiles;      // output tiles [0, tri_tiles) come from a lower-triangular B (CLAK-Chol's L^-1): K < (tn+1)*64
 };
 
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
@@ -201,7 +202,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   }
   const int m0 = tm * I8_BM;
   const int brow0 = tn * I8_BROWS;
-  const int KB = (s.K + I8_BKB - 1) / I8_BKB;
+  const int k_end = tn < s.tri_tiles ? min(s.K, (tn + 1) * I8_NB) : s.K;
+  const int KB = (k_end + I8_BKB - 1) / I8_BKB;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < I8_STAGES; ++i) {
@@ -348,7 +350,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   }
   const int m0 = tm * I8_BM;
   const int brow0 = tn * I8_BROWS;
-  const int KB = (s.K + I8_BKB - 1) / I8_BKB;
+  const int k_end = tn < s.tri_tiles ? min(s.K, (tn + 1) * I8_NB) : s.K;
+  const int KB = (k_end + I8_BKB - 1) / I8_BKB;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < I8_STAGES2; ++i) {
@@ -459,6 +462,23 @@ __global__ void digitize_rows(const double* __restrict__ X, long long ldx, int r
       v = (v - d) * 128.0;  // exact: |v - d| <= 1/2
     }
   }
+}
+
+// CLAK-Chol setup (Alg. 3 line 1): M = sigma2 (h2 Phi + (1 - h2) I) in place over a copy of Phi
+// (column-major, ld kpad), both triangles from one expression per entry.
+__global__ void assemble_m(double* __restrict__ A, int n, int kpad, double sigma2, double h2) {
+  const int c = blockIdx.y;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const double phi = A[(long long)c * kpad + r];
+    A[(long long)c * kpad + r] = sigma2 * (h2 * phi + (r == c ? 1.0 - h2 : 0.0));
+  }
+}
+
+// Zero the strict upper triangle (and the padding) of a column-major kpad x kpad matrix (dtrtri leaves M there).
+__global__ void zero_upper(double* __restrict__ A, int n, int kpad) {
+  const int c = blockIdx.y;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < kpad; r += gridDim.x * blockDim.x)
+    if (r < c || r >= n || c >= n) A[(long long)c * kpad + r] = 0.0;
 }
 
 // Out-of-place transpose of a kpad x kpad fp64 matrix (tiled through shared memory).

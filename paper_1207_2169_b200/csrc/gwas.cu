@@ -68,7 +68,7 @@ struct StateHeader {
   int32_t output_mode, var_convention;
   double eps_collinear;
   int64_t off_Z, off_W, off_B2, off_Lpk, off_v, off_s2, off_betaT, off_dinv, total;
-  int32_t int8_slices, pad0;
+  int32_t int8_slices, algorithm;
   int64_t na_pad, nlin, nlin_pad, off_dig, off_exps;  // int8-sliced mode: digit matrix of [Z | Z B_op] + 2^e
 };
 constexpr size_t kHeaderBytes = 512;
@@ -130,6 +130,7 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
   h.off_betaT = take(sizeof(double) * d.p * d.t);
   h.off_dinv = take(sizeof(double) * d.p * d.t);
   h.int8_slices = o->int8_slices;
+  h.algorithm = o->algorithm;
   h.na_pad = d.na_pad;
   h.nlin = d.nlin;
   h.nlin_pad = d.nlin_pad;
@@ -209,6 +210,9 @@ gwas_status check_sizes(int64_t n, int64_t p, int64_t t, const gwas_options* o) 
   if (!(o->eps_spd >= 0) || !(o->eps_collinear >= 0)) return fail(GWAS_E_ARG, "bad eps");
   const int64_t t_p2 = t * (p + 2) + 8;
   if (t_p2 > (1ll << 31) - 1) return fail(GWAS_E_ARG, "t too large");
+  if (o->algorithm != GWAS_ALG_EIG && o->algorithm != GWAS_ALG_CHOL) return fail(GWAS_E_ARG, "bad algorithm");
+  if (o->algorithm == GWAS_ALG_CHOL && t != 1)
+    return fail(GWAS_E_ARG, "CLAK-Chol (Alg. 3) is the single-trait algorithm: t = %lld != 1", (long long)t);
   if (o->int8_slices != 0) {
     if (o->int8_slices != gw::I8_SLICES)
       return fail(GWAS_E_ARG, "int8_slices = %d unsupported (0 or %d)", o->int8_slices, gw::I8_SLICES);
@@ -218,16 +222,31 @@ gwas_status check_sizes(int64_t n, int64_t p, int64_t t, const gwas_options* o) 
   return GWAS_OK;
 }
 
-gwas_status dsyevd_lwork(int device, int64_t n, int64_t kpad, int64_t* lwork) {
-  CKC(cudaSetDevice(device));
+// Device workspace (in doubles) of the setup factorisation: dsyevd (CLAK-Eig), or for CLAK-Chol the n x n matrix M
+// (kpad x kpad) followed by max(dpotrf, dtrtri) workspace.  *host_bytes: dtrtri's host workspace.
+gwas_status solver_lwork(const gwas_options* o, int64_t n, int64_t kpad, int64_t* lwork, size_t* host_bytes) {
+  CKC(cudaSetDevice(o->device));
   cusolverDnHandle_t h;
   CKS(cusolverDnCreate(&h));
-  int lw = 0;
-  cusolverStatus_t s = cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n,
-                                                   nullptr, (int)kpad, nullptr, &lw);
+  *host_bytes = 0;
+  cusolverStatus_t s = CUSOLVER_STATUS_SUCCESS;
+  if (o->algorithm == GWAS_ALG_CHOL) {
+    int lw = 0;
+    size_t dev_b = 0, host_b = 0;
+    s = cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)n, nullptr, (int)kpad, &lw);
+    if (s == CUSOLVER_STATUS_SUCCESS)
+      s = cusolverDnXtrtri_bufferSize(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, nullptr, kpad,
+                                      &dev_b, &host_b);
+    *lwork = kpad * kpad + std::max<int64_t>(lw, (int64_t)((dev_b + 7) / 8)) + 64;
+    *host_bytes = host_b;
+  } else {
+    int lw = 0;
+    s = cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, nullptr, (int)kpad,
+                                    nullptr, &lw);
+    *lwork = lw;
+  }
   cusolverDnDestroy(h);
-  if (s != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "dsyevd_bufferSize status %d", (int)s);
-  *lwork = lw;
+  if (s != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "cuSOLVER bufferSize status %d", (int)s);
   return GWAS_OK;
 }
 
@@ -297,7 +316,7 @@ gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw
 constexpr int kSplitMax = 8, kSplitLd = 64;
 gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                     int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st, int group_m = 16,
-                    double* split_scratch = nullptr) {
+                    double* split_scratch = nullptr, bool tri = false) {
   if (M <= 0 || N <= 0) return GWAS_OK;
   if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
   if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
@@ -328,6 +347,7 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.ksplit = 1;
   s.kt_per_split = kt_all;
   s.split_stride = 0;
+  s.tri = tri ? 1 : 0;
   double* c_final = C;
   int64_t ldc_final = ldc;
   if (split_scratch && N <= kSplitLd && kt_all >= 16) {
@@ -391,7 +411,7 @@ gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
 // K1i/K2a: C_a[i][c] (c < na) and C_b[i][c'] (c' < nb) from the u8 A block and the stacked digit matrix.
 gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const int8_t* dig, int64_t ldd,
                       int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
-                      double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st) {
+                      double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st, int64_t tri_tiles = 0) {
   if (M <= 0) return GWAS_OK;
   // GWAS_I8_KERNEL: "1sm" (default) with GWAS_I8_CLUSTER (1, 2 or 4; default 2) CTAs multicasting the digit
   // slab, or "2sm" (CTA pairs with cta_group::2 MMAs).  Measured at C4 per 8192-column block: 1sm x1 14.4 ms,
@@ -425,6 +445,7 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   s.ldb_c = ldcb;
   s.exps = exps;
   s.group_m = 64;
+  s.tri_tiles = (int)tri_tiles;
   constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256;
   constexpr size_t smem2 = 1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256;
   static bool attr_set = false;
@@ -612,7 +633,8 @@ size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options*
   if (check_sizes(n, p, t, o) != GWAS_OK) return 0;
   Dims d = make_dims(n, p, t, o);
   int64_t lwork = 0;
-  if (dsyevd_lwork(o->device, n, d.kpad, &lwork) != GWAS_OK) return 0;
+  size_t host_ws = 0;
+  if (solver_lwork(o, n, d.kpad, &lwork, &host_ws) != GWAS_OK) return 0;
   return std::max(setup_layout(d, lwork).total, run_layout(d, o->overlap != 0).total);
 }
 
@@ -628,7 +650,8 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
   Dims d = make_dims(n, p, t, o);
   StateHeader h = make_header(d, o);
   int64_t lwork = 0;
-  CKG(dsyevd_lwork(o->device, n, d.kpad, &lwork));
+  size_t host_ws = 0;
+  CKG(solver_lwork(o, n, d.kpad, &lwork, &host_ws));
   SetupLayout sl = setup_layout(d, lwork);
   RunLayout rl = run_layout(d, o->overlap != 0);
   if (state_bytes < (size_t)h.total) return fail(GWAS_E_NOMEM, "state %zu < %lld bytes", state_bytes, (long long)h.total);
@@ -685,21 +708,60 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     CKC(cudaMemcpy2DAsync(ypad, sizeof(double) * d.kpad, Y, sizeof(double) * n, sizeof(double) * n, t,
                           cudaMemcpyDefault, cs));
     CKC(cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long) * 4, cs));
-    // Alg. 4 line 1: Phi = Z W Z^T, in place (Z overwrites Phi)
     CKC(cudaEventRecord(e1, cs));
     cusolverDnHandle_t hs;
     CKS(cusolverDnCreate(&hs));
     cusolverStatus_t ss2 = cusolverDnSetStream(hs, cs);
-    if (ss2 == CUSOLVER_STATUS_SUCCESS)
-      ss2 = cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, c->Z(), (int)d.kpad,
-                             c->W(), dwork, (int)lwork, dinfo);
+    const bool chol = o->algorithm == GWAS_ALG_CHOL;
+    std::vector<uint8_t> host_ws_buf(std::max<size_t>(host_ws, 1));
+    if (!chol) {
+      // Alg. 4 line 1: Phi = Z W Z^T, in place (Z overwrites Phi)
+      if (ss2 == CUSOLVER_STATUS_SUCCESS)
+        ss2 = cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, c->Z(), (int)d.kpad,
+                               c->W(), dwork, (int)lwork, dinfo);
+    } else {
+      // Alg. 3 lines 1-2: M = sigma2 (h2 Phi + (1 - h2) I) = L L^T, then L^-1 (dtrtri) so that
+      // line 4, X_R := L^-1 X_R, is a (lower-triangular) product; the state's rotation R = L^-1 stored by rows.
+      double* Mw = dwork;
+      double* sw = dwork + d.kpad * d.kpad;
+      const int64_t slw = lwork - d.kpad * d.kpad;
+      CKC(cudaMemcpy2DAsync(Mw, sizeof(double) * d.kpad, c->Z(), sizeof(double) * d.kpad, sizeof(double) * d.kpad,
+                            d.kpad, cudaMemcpyDeviceToDevice, cs));
+      gw::assemble_m<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n), 256, 0, cs>>>(
+          Mw, (int)n, (int)d.kpad, ss[0], hh[0]);
+      CKC(cudaGetLastError());
+      if (ss2 == CUSOLVER_STATUS_SUCCESS)
+        ss2 = cusolverDnDpotrf(hs, CUBLAS_FILL_MODE_LOWER, (int)n, Mw, (int)d.kpad, sw, (int)slw, dinfo);
+      CKC(cudaStreamSynchronize(cs));
+      int pinfo = 0;
+      CKC(cudaMemcpy(&pinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+      if (ss2 == CUSOLVER_STATUS_SUCCESS && pinfo != 0) {
+        cusolverDnDestroy(hs);
+        return fail(GWAS_E_NOT_SPD, "trait 0: M = sigma2 (h2 Phi + (1 - h2) I) not positive definite (dpotrf info %d)",
+                    pinfo);
+      }
+      if (ss2 == CUSOLVER_STATUS_SUCCESS)
+        ss2 = cusolverDnXtrtri(hs, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, Mw, d.kpad, sw,
+                               (size_t)slw * sizeof(double), host_ws_buf.data(), host_ws, dinfo);
+      gw::zero_upper<<<dim3((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)d.kpad), 256, 0, cs>>>(
+          Mw, (int)n, (int)d.kpad);
+      CKC(cudaGetLastError());
+      gw::transpose_sq<<<dim3((unsigned)((d.kpad + 31) / 32), (unsigned)((d.kpad + 31) / 32)), dim3(32, 8), 0, cs>>>(
+          Mw, c->Z(), (int)d.kpad);
+      CKC(cudaGetLastError());
+      // D = I: the trait's M^-1 is applied through L^-1 already (K2 weights d = 1 via h2 = 0, sigma2 = 1)
+      CKC(cudaMemsetAsync(dh2, 0, sizeof(double) * t, cs));
+      const double one = 1.0;
+      CKC(cudaMemcpyAsync(ds2, &one, sizeof(double), cudaMemcpyHostToDevice, cs));
+    }
     CKC(cudaEventRecord(e2, cs));
     CKC(cudaStreamSynchronize(cs));
     cusolverDnDestroy(hs);
-    if (ss2 != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "cusolverDnDsyevd status %d", (int)ss2);
+    if (ss2 != CUSOLVER_STATUS_SUCCESS)
+      return fail(GWAS_E_CUDA, "cuSOLVER %s status %d", chol ? "dpotrf/dtrtri" : "dsyevd", (int)ss2);
     int info = 0;
     CKC(cudaMemcpy(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
-    if (info != 0) return fail(GWAS_E_EIG, "dsyevd info = %d", info);
+    if (info != 0) return fail(GWAS_E_EIG, "%s info = %d", chol ? "dtrtri" : "dsyevd", info);
     // Alg. 4 lines 2, 4: X_L' = Z^T X_L, Y' = Z^T Y  (K1 kernel, fp64 A)
     CKG(gemm_tn(false, xlpad, d.kpad, c->Z(), d.kpad, xlp, d.kpad, p, n, n, n, cs));
     CKG(gemm_tn(false, ypad, d.kpad, c->Z(), d.kpad, yp, d.kpad, t, n, n, n, cs));
@@ -783,7 +845,7 @@ gwas_status gwas_attach(const gwas_options* o, int64_t n, int64_t p, int64_t t, 
   CKC(cudaMemcpy(&got, state_dev, sizeof(got), cudaMemcpyDeviceToHost));
   if (got.magic != kMagic || got.version != kVersion || got.n != n || got.p != p || got.t != t ||
       got.total != want.total || got.output_mode != o->output_mode || got.var_convention != o->var_convention ||
-      got.int8_slices != o->int8_slices)
+      got.int8_slices != o->int8_slices || got.algorithm != o->algorithm)
     return fail(GWAS_E_STATE, "state header does not match (n, p, t, options)");
   gwas_ctx* c = new gwas_ctx();
   gwas_status st = ctx_init(c, o, d, got, state_dev, work_dev, work_bytes);
@@ -809,6 +871,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
   if (dev && (((ldx * (int64_t)d.es) & 15) || (reinterpret_cast<uintptr_t>(XR) & 15)))
     return fail(GWAS_E_ARG, "device X_R: ldx * elem_size must be a multiple of 16 and XR 16-byte aligned");
   const bool u8 = c->opt.xr_dtype == GWAS_XR_U8;
+  const bool chol = c->opt.algorithm == GWAS_ALG_CHOL;
   const int64_t w = d.p + 1;
   const int64_t per_pair = c->opt.output_mode == GWAS_OUT_FULL ? w : 1;
   cudaStream_t cs = c->cs, ps = c->ps;
@@ -853,7 +916,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     if (!d.i8) {
       // K1 (Alg. 4 line 3): X_R'^T = X_R^T Z  (row i of xrp = Z^T g_i)
       CKG(c->tic(GWAS_K1, cs, &dummy));
-      CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64));
+      CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64, nullptr, chol));
       CKG(c->toc(cs));
       if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
       if (ovl) {
@@ -868,7 +931,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       // K1i + K2a (int8-sliced, exact): X_R'^T = X_R^T Z and C[:, 0:t(p+1)] = X_R^T (Z B_op) in one launch
       CKG(c->tic(GWAS_K1, cs, &dummy));
       CKG(launch_i8(A, lda, cols, d.n, c->dig(), d.kpad, (d.na_pad + d.nlin_pad) / gw::I8_NB, d.na_pad / gw::I8_NB,
-                    c->exps(), xrp, d.kpad, d.n, c2, d.ldc2, d.nlin, cs));
+                    c->exps(), xrp, d.kpad, d.n, c2, d.ldc2, d.nlin, cs, chol ? d.na_pad / gw::I8_NB : 0));
       CKG(c->toc(cs));
       if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
       if (ovl) {

@@ -41,3 +41,29 @@ def test_full_config_subsample(index, i8):
           f"max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
     assert snps.size * traits.size >= 10_000
     assert eb <= TOL_B and ev <= TOL_VAR
+
+
+@pytest.mark.parametrize("index,i8", [(1, 0), (3, 0), (1, 8), (3, 8)])
+def test_full_config_subsample_chol(index, i8):
+    """The single-trait configs through CLAK-Chol (Alg. 3) at full size, in both K1 modes."""
+    import paper_1207_2169_b200 as gw
+    cfg = datagen.CONFIGS[index]
+    dev = torch.device("cuda", 0)
+    ds = datagen.dataset(cfg, device=dev)
+    ld = (cfg.n + 15) // 16 * 16
+    xr = torch.empty((cfg.m, ld), dtype=torch.uint8, pin_memory=True)
+    datagen.xr_dosages(cfg, ld=ld, out=xr.numpy())
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=8192, int8_slices=i8, algorithm="chol", overlap=True)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    b, v, s = eng.run(xr.to(dev))
+    snps, traits = datagen.subsample(cfg)
+    idx_s = torch.from_numpy(snps).to(dev)
+    bs = b.index_select(0, idx_s).cpu().numpy()
+    vs = v.index_select(0, idx_s).cpu().numpy()
+    ss = s.index_select(0, idx_s).cpu().numpy()
+    eng.close()
+    G = datagen.xr_columns(cfg, snps)
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
+    eb, ev = compare(bs, vs, ss, ref)
+    print(f"C{index} chol int8_slices={i8}: {snps.size} pairs, max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
+    assert eb <= TOL_B and ev <= TOL_VAR

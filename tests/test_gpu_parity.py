@@ -378,3 +378,38 @@ def test_split_k_skinny_products(i8):
     b2, v2, s2 = _run(cfg, ds, torch.from_numpy(XR).cuda(), int8_slices=i8, block_cols=300, overlap=True)
     np.testing.assert_array_equal(b, b2)
     np.testing.assert_array_equal(v, v2)
+
+
+# ------------------------------------------------------------------ CLAK-Chol single-trait path (Alg. 3, NEXT-1)
+@pytest.mark.parametrize("i8,n,mode,k", [(0, 200, "snp", 2000), (8, 200, "full", 512), (0, 333, "full", 256),
+                                         (8, 333, "snp", 100), (0, 4100, "snp", 256), (8, 4100, "snp", 300)])
+def test_chol_single_trait(i8, n, mode, k):
+    cfg = datagen.custom_config(n=n, p=4, m=600 if n < 1000 else 200, t=1, index=800 + n)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), algorithm="chol", int8_slices=i8, output_mode=mode,
+                   block_cols=k)
+    eb, ev = compare(b, v, s, ref, full=(mode == "full"))
+    print(f"chol n={n} int8={i8}: max|db|/SE={eb:.3e} max Var rel={ev:.3e}")
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+    if mode == "snp":   # block size / overlap invariance (bitwise)
+        b2, v2, s2 = _run(cfg, ds, torch.from_numpy(XR).cuda(), algorithm="chol", int8_slices=i8, block_cols=k + 37,
+                          overlap=True)
+        np.testing.assert_array_equal(b, b2)
+        np.testing.assert_array_equal(v, v2)
+
+
+def test_chol_errors():
+    gw = _gw()
+    with pytest.raises(gw.GwasError) as e:
+        gw.Gwas(64, 3, 2, device=0, algorithm="chol")
+    assert e.value.code == 1
+    cfg = datagen.custom_config(n=64, p=3, m=10, t=1, index=802)
+    ds = datagen.dataset(cfg)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, algorithm="chol")
+    with pytest.raises(gw.GwasError) as e:   # h2 = 1 with the singular sample-centred GRM: M not SPD
+        eng.setup(ds.Phi, ds.XL, ds.Y, np.array([1.0]), ds.s2)
+    assert e.value.code == 2
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    eng.close()
