@@ -233,9 +233,10 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    def make_engine(i8, overlap):
+    def make_engine(i8, overlap, algorithm="eig"):
         """Rank 0 sets up (eig + precompute), the state is replicated by ONE broadcast, other ranks attach."""
-        eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=overlap)
+        eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=overlap,
+                      algorithm=algorithm)
         info = {}
         if rank == 0:
             eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
@@ -252,7 +253,8 @@ def run_ours(args):
             if rank != 0:
                 eng.attach()
         # a second, serial context on the same state (gwas_attach) times the kernels one by one
-        ser = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=False)
+        ser = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=False,
+                      algorithm=algorithm)
         ser.state.copy_(eng.state)
         ser.attach()
         return eng, ser, info
@@ -347,12 +349,40 @@ def run_ours(args):
         eng8.close()
         ser8.close()
 
+    # ================= CLAK-Chol single-trait path (Alg. 3, NEXT-1), t == 1 only =================
+    chol_modes, chol_res = {}, []
+    if t == 1 and args.chol_alt:
+        for i8 in (0, 8):
+            engc, serc, setupc = make_engine(i8, True, "chol")
+            for _ in range(args.warmup):
+                engc.run(xr_dev, out=out)
+            msc = max_over_ranks(_timed_steps(engc, xr_dev, out, args.steps, engc.compute_stream, barrier), world,
+                                 dev)
+            ktc = _kernel_pass(serc, xr_dev, out, args.kernel_steps, barrier)
+            c1_ms = ktc["K1"]["ms"] / args.kernel_steps
+            tri_flops = sum(1.0 * n * n * c for c in blocks)   # L^-1 X_R: n^2 k (half of 2 n^2 k)
+            entry = {"value": pairs_total * args.steps / (msc / 1e3), "unit": UNIT, "ms_per_step": msc / args.steps,
+                     "K1_ms_per_step": c1_ms, "setup": setupc,
+                     "K1_tflops_algorithmic": tri_flops / (c1_ms / 1e3) / 1e12}
+            if i8 == 0:
+                entry["K1_frac_of_fp64_peak"] = entry["K1_tflops_algorithmic"] / peak
+            chol_modes["chol_int8_sliced" if i8 else "chol_fp64"] = entry
+            if args.check and rank == 0:
+                torch.cuda.synchronize(dev)
+                chol_res.append((out[0].cpu().numpy(), out[1].cpu().numpy(), out[2].cpu().numpy()))
+            engc.close()
+            serc.close()
+
     # ---------------- parity spot check on this run's outputs (outside timed regions)
     parity = None
     if args.check and rank == 0:
-        parity = spot_check(cfg, gcfg, ds, lo, hi, [res_fp64] + ([alt_res] if alt is not None else []), args.check)
+        parity = spot_check(cfg, gcfg, ds, lo, hi, [res_fp64] + ([alt_res] if alt is not None else []) + chol_res,
+                            args.check)
+        extra = parity.pop("extra")
         if alt is not None:
-            alt["parity"] = parity.pop("extra")[0]
+            alt["parity"] = extra.pop(0)
+        for name, pr in zip(list(chol_modes), extra):
+            chol_modes[name]["parity"] = pr
 
     res = None
     if rank == 0:
@@ -385,8 +415,9 @@ def run_ours(args):
             "setup": {**setup, "datagen_s": t_gen},
             "clocks": clocks,
         }
-        if alt is not None:
-            res["modes"] = {"int8_sliced": alt}
+        if alt is not None or chol_modes:
+            res["modes"] = ({"int8_sliced": alt} if alt is not None else {})
+            res["modes"].update(chol_modes)
         if parity is not None:
             res["parity"] = parity
         if not args.no_cpu_baseline:
@@ -480,6 +511,8 @@ def main(argv=None):
     ap.add_argument("--snps", type=int, default=None, help="override m per rank (testing only)")
     ap.add_argument("--overlap", type=int, default=1, help="1: pipeline block b's K2/K3 beside block b+1's K1")
     ap.add_argument("--kernel-steps", type=int, default=1, help="serial passes timed per kernel (roofline)")
+    ap.add_argument("--no-chol-alt", dest="chol_alt", action="store_false",
+                    help="skip the CLAK-Chol (Alg. 3) modes reported under `modes` for single-trait configs")
     ap.add_argument("--no-int8-alt", dest="int8_alt", action="store_false",
                     help="skip the int8-sliced mode measurement reported under `modes`")
     ap.add_argument("--e2e-steps", type=int, default=2)
