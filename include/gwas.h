@@ -16,8 +16,9 @@
  *
  * Conventions (all calls):
  *   - Matrices are column-major fp64 unless stated; sizes are int64_t; "ld" = leading dimension in elements.
- *   - The caller owns every buffer (state, workspace, outputs) and every stream; the library allocates no
- *     device memory (a cuSOLVER handle is created inside gwas_setup only).
+ *   - The caller owns every buffer (state, workspace, outputs) and the compute / copy streams; the library
+ *     allocates no device memory (a cuSOLVER handle is created inside gwas_setup only).  Each context creates
+ *     and owns two internal streams: the overlap-mode auxiliary stream and the D2H stream for host outputs.
  *   - Pointers documented "host or device" are classified with cudaPointerGetAttributes.
  *   - Calls enqueue on options.compute_stream (and options.copy_stream for staging) and return without
  *     synchronising, except gwas_setup / gwas_attach, which synchronise to report errors.
@@ -81,7 +82,7 @@ typedef struct {
                               W_R^T W_R term stays on DMMA.  Fixed at setup (part of the state). */
   int32_t overlap;         /* 1 = pipeline blocks over two streams: block b's K2 + K3 run on an internal auxiliary
                               stream while block b+1's K1 runs on compute_stream (double-buffered intermediates;
-                              the library creates and owns that one stream).  gwas_run still completes on
+                              the stream is created and owned by the context).  gwas_run still completes on
                               compute_stream.  Per-kernel event times then overlap.  Default 0. */
   int32_t algorithm;       /* GWAS_ALG_EIG (default): CLAK-Eig, Alg. 4, any t.
                               GWAS_ALG_CHOL: CLAK-Chol single-trait analysis, Alg. 3, t == 1 only:
@@ -127,10 +128,13 @@ GWAS_API gwas_status gwas_attach(const gwas_options* opt, int64_t n, int64_t p, 
  *          Device pointer: ldx * sizeof(elem) must be a multiple of 16 and the address 16-byte aligned.
  *          Host pointer: must be page-locked (cudaHostAlloc / cudaHostRegister); blocks of block_cols
  *          columns are staged to HBM on copy_stream, double-buffered against compute (any ldx >= n).
- *   b, var (device) ncols x t row-major ([i][j], trait fastest) in GWAS_OUT_SNP mode, or
+ *   b, var, status: all device memory, or all page-locked host memory (then each block's results are staged in
+ *          the workspace and copied to the host on an internal D2H stream while later blocks compute -- the
+ *          output side of the paper's double buffering).
+ *   b, var ncols x t row-major ([i][j], trait fastest) in GWAS_OUT_SNP mode, or
  *          ncols x t x w ([i][j][e], e = 0..p-1 the X_L coefficients, e = p the SNP) in GWAS_OUT_FULL mode;
  *          var holds Var_gg (SNP mode) or the diagonal of Var (full mode).
- *   status (device) ncols x t int8 (GWAS_PAIR_*).
+ *   status ncols x t int8 (GWAS_PAIR_*).
  * Asynchronous on compute_stream; XR and the outputs must stay valid until it completes. */
 GWAS_API gwas_status gwas_run(gwas_ctx* ctx, int64_t ncols, const void* XR, int64_t ldx,
                      double* b, double* var, int8_t* status);

@@ -107,16 +107,20 @@ class Gwas:
         return self
 
     # ------------------------------------------------------------------ hot path
-    def alloc_outputs(self, ncols: int):
+    def alloc_outputs(self, ncols: int, host: bool = False):
+        """(b, var, status) buffers: on the device, or in pinned host memory (host=True) -- then gwas_run streams
+        each block's results back while later blocks compute."""
         per = (self.w,) if self.output_mode == "full" else ()
-        b = torch.empty((ncols, self.t) + per, dtype=torch.float64, device=self.device)
-        v = torch.empty((ncols, self.t) + per, dtype=torch.float64, device=self.device)
-        s = torch.empty((ncols, self.t), dtype=torch.int8, device=self.device)
+        kw = dict(pin_memory=True) if host else dict(device=self.device)
+        b = torch.empty((ncols, self.t) + per, dtype=torch.float64, **kw)
+        v = torch.empty((ncols, self.t) + per, dtype=torch.float64, **kw)
+        s = torch.empty((ncols, self.t), dtype=torch.int8, **kw)
         return b, v, s
 
     def run(self, XR, ldx: int | None = None, ncols: int | None = None, out=None):
         """X_R (ncols, ld) SNP-major: torch cuda tensor, or pinned host torch tensor (staged on copy_stream).
-        Returns (b, var, status) device tensors; asynchronous on compute_stream."""
+        Returns (b, var, status) -- device tensors, or the pinned host tensors passed as `out`; asynchronous on
+        compute_stream."""
         if not self._ctx:
             raise _lib.GwasError(_lib.GWAS_E_STATE, "setup()/attach() first")
         if isinstance(XR, np.ndarray):

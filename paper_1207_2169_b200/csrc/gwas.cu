@@ -77,6 +77,7 @@ static_assert(sizeof(StateHeader) <= kHeaderBytes, "header");
 struct Dims {
   int64_t n, p, t, kpad, nsq, n2, ldc2, lds, kb;
   size_t es;
+  int64_t per_pair;                // outputs per pair: 1 (SNP mode) or p + 1 (full mode)
   int i8;                          // int8-sliced mode
   int64_t na_pad, nlin, nlin_pad;  // digit-matrix column blocks (multiples of 64)
 };
@@ -94,6 +95,7 @@ Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   d.kb = o->block_cols > 0 ? o->block_cols : 8192;
   d.es = o->xr_dtype == GWAS_XR_U8 ? 1 : 8;
   d.i8 = o->int8_slices != 0;
+  d.per_pair = o->output_mode == GWAS_OUT_FULL ? p + 1 : 1;
   d.na_pad = round_up(n, gw::I8_NB);
   d.nlin = t * (p + 1);
   d.nlin_pad = round_up(d.nlin, gw::I8_NB);
@@ -143,7 +145,8 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
 }
 
 struct RunLayout {
-  size_t stage[2], xrp[2], c2[2], split[2], total;
+  size_t stage[2], xrp[2], c2[2], split[2], outb[2], total;
+  size_t out_bytes;  // per staging set: b, var (8 * per_pair each) + status (1) per pair of a block
 };
 // overlap mode double-buffers the rotated block and the K2 output so block b+1's K1 can run beside block b's K2/K3
 RunLayout run_layout(const Dims& d, bool overlap) {
@@ -162,6 +165,10 @@ RunLayout run_layout(const Dims& d, bool overlap) {
   r.c2[1] = overlap ? take(sizeof(double) * d.ldc2 * d.kb) : r.c2[0];
   r.split[0] = take(sizeof(double) * 8 * 64 * d.kb);  // split-K partials of skinny K2 products (kSplitMax x kSplitLd)
   r.split[1] = overlap ? take(sizeof(double) * 8 * 64 * d.kb) : r.split[0];
+  // host-output mode: each block's b / var / status land here and stream to pinned host memory on the D2H stream
+  r.out_bytes = (size_t)d.kb * d.t * (16 * d.per_pair + 1);
+  r.outb[0] = take(r.out_bytes);
+  r.outb[1] = take(r.out_bytes);
   r.total = off;
   return r;
 }
@@ -513,6 +520,8 @@ struct gwas_ctx {
   cudaStream_t aux = nullptr;  // overlap mode: K2 + K3 of block b beside K1 of block b+1 (owned by the context)
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   cudaEvent_t ev_k1[2] = {nullptr, nullptr}, ev_set_free[2] = {nullptr, nullptr}, ev_join = nullptr;
+  cudaStream_t dstream = nullptr;  // D2H of results when the caller's outputs are pinned host memory
+  cudaEvent_t ev_out_ready[2] = {nullptr, nullptr}, ev_out_free[2] = {nullptr, nullptr}, ev_djoin = nullptr;
   int stage_next = 0;
   bool stage_zeroed = false;
   float ms_eig = 0.f, ms_pre = 0.f;
@@ -597,6 +606,12 @@ gwas_status ctx_init(gwas_ctx* c, const gwas_options* o, const Dims& d, const St
     CKC(cudaEventCreateWithFlags(&c->ev_set_free[i], cudaEventDisableTiming));
   }
   CKC(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&c->ev_djoin, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    CKC(cudaEventCreateWithFlags(&c->ev_out_ready[i], cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_out_free[i], cudaEventDisableTiming));
+  }
+  CKC(cudaStreamCreateWithFlags(&c->dstream, cudaStreamNonBlocking));
   if (o->overlap) CKC(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   return GWAS_OK;
 }
@@ -870,6 +885,11 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
   if (!dev && !is_pinned_host(XR)) return fail(GWAS_E_ARG, "X_R host buffer is not page-locked (use pinned memory)");
   if (dev && (((ldx * (int64_t)d.es) & 15) || (reinterpret_cast<uintptr_t>(XR) & 15)))
     return fail(GWAS_E_ARG, "device X_R: ldx * elem_size must be a multiple of 16 and XR 16-byte aligned");
+  const bool out_dev = is_device_ptr(b);
+  if (is_device_ptr(var) != out_dev || is_device_ptr(status) != out_dev)
+    return fail(GWAS_E_ARG, "b, var and status must all be device memory or all pinned host memory");
+  if (!out_dev && !(is_pinned_host(b) && is_pinned_host(var) && is_pinned_host(status)))
+    return fail(GWAS_E_ARG, "host outputs must be page-locked (pinned)");
   const bool u8 = c->opt.xr_dtype == GWAS_XR_U8;
   const bool chol = c->opt.algorithm == GWAS_ALG_CHOL;
   const int64_t w = d.p + 1;
@@ -959,17 +979,39 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     a.eps_collinear = c->opt.eps_collinear;
     a.literal = c->opt.var_convention == GWAS_VAR_LITERAL;
     a.full = c->opt.output_mode == GWAS_OUT_FULL;
-    a.b = b + blk * d.t * per_pair;
-    a.var = var + blk * d.t * per_pair;
-    a.status = status + blk * d.t;
+    const int oset = (int)(bi & 1);
+    uint8_t* ob = c->work + c->rl.outb[oset];
+    if (out_dev) {
+      a.b = b + blk * d.t * per_pair;
+      a.var = var + blk * d.t * per_pair;
+      a.status = status + blk * d.t;
+    } else {  // results of block bi-2 must have left this staging set
+      CKC(cudaStreamWaitEvent(cs2, c->ev_out_free[oset], 0));
+      a.b = reinterpret_cast<double*>(ob);
+      a.var = a.b + cols * d.t * per_pair;
+      a.status = reinterpret_cast<int8_t*>(a.var + cols * d.t * per_pair);
+    }
     CKG(c->tic(GWAS_K3, cs2, &dummy));
     CKG(launch_schur(a, (int)d.p, cs2));
     CKG(c->toc(cs2));
     if (ovl) CKC(cudaEventRecord(c->ev_set_free[set], cs2));
+    if (!out_dev) {  // stream this block's results to the caller's pinned host buffers, overlapped with compute
+      CKC(cudaEventRecord(c->ev_out_ready[oset], cs2));
+      CKC(cudaStreamWaitEvent(c->dstream, c->ev_out_ready[oset], 0));
+      const size_t nb = sizeof(double) * cols * d.t * per_pair;
+      CKC(cudaMemcpyAsync(b + blk * d.t * per_pair, a.b, nb, cudaMemcpyDeviceToHost, c->dstream));
+      CKC(cudaMemcpyAsync(var + blk * d.t * per_pair, a.var, nb, cudaMemcpyDeviceToHost, c->dstream));
+      CKC(cudaMemcpyAsync(status + blk * d.t, a.status, (size_t)cols * d.t, cudaMemcpyDeviceToHost, c->dstream));
+      CKC(cudaEventRecord(c->ev_out_free[oset], c->dstream));
+    }
   }
   if (ovl) {  // join: the call completes on compute_stream
     CKC(cudaEventRecord(c->ev_join, cs2));
     CKC(cudaStreamWaitEvent(cs, c->ev_join, 0));
+  }
+  if (!out_dev) {
+    CKC(cudaEventRecord(c->ev_djoin, c->dstream));
+    CKC(cudaStreamWaitEvent(cs, c->ev_djoin, 0));
   }
   return GWAS_OK;
 }
@@ -1016,6 +1058,15 @@ void gwas_destroy(gwas_ctx* c) {
     if (c->ev_set_free[i]) cudaEventDestroy(c->ev_set_free[i]);
   }
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_djoin) cudaEventDestroy(c->ev_djoin);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_out_ready[i]) cudaEventDestroy(c->ev_out_ready[i]);
+    if (c->ev_out_free[i]) cudaEventDestroy(c->ev_out_free[i]);
+  }
+  if (c->dstream) {
+    cudaStreamSynchronize(c->dstream);
+    cudaStreamDestroy(c->dstream);
+  }
   if (c->aux) {
     cudaStreamSynchronize(c->aux);
     cudaStreamDestroy(c->aux);

@@ -413,3 +413,22 @@ def test_chol_errors():
     assert e.value.code == 2
     eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
     eng.close()
+
+
+@pytest.mark.parametrize("i8,ovl,mode", [(0, False, "snp"), (0, True, "full"), (8, True, "snp")])
+def test_host_outputs_stream_back(c0, i8, ovl, mode):
+    """Pinned host outputs (per-block D2H on the library's stream) equal device outputs bitwise."""
+    cfg, ds, XR, _ = c0
+    gw = _gw()
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, int8_slices=i8, overlap=ovl, output_mode=mode, block_cols=300)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    dev = [x.cpu().numpy() for x in eng.run(torch.from_numpy(XR).cuda())]
+    host = eng.alloc_outputs(cfg.m, host=True)
+    eng.run(torch.from_numpy(XR).pin_memory(), out=host)
+    torch.cuda.synchronize()
+    for x, y in zip(dev, host):
+        np.testing.assert_array_equal(x, y.numpy())
+    mixed = (host[0], host[1], torch.empty((cfg.m, cfg.t), dtype=torch.int8, device="cuda"))
+    with pytest.raises(gw.GwasError):
+        eng.run(torch.from_numpy(XR).cuda(), out=mixed)
+    eng.close()
