@@ -63,6 +63,7 @@ enum { GWAS_VAR_TEXTBOOK = 0, GWAS_VAR_LITERAL = 1 };
 enum { GWAS_PAIR_OK = 0, GWAS_PAIR_COLLINEAR = 1, GWAS_PAIR_NONFINITE = 2 };
 enum { GWAS_K1 = 0, GWAS_K2 = 1, GWAS_K3 = 2, GWAS_H2D = 3, GWAS_NUM_TIMERS = 4 };
 enum { GWAS_ALG_EIG = 0, GWAS_ALG_CHOL = 1 };
+enum { GWAS_EST_ML = 0, GWAS_EST_REML = 1 };         /* variance-component estimator (gwas_setup_estimate) */
 
 typedef struct {
   int32_t device;          /* CUDA ordinal the context binds to */
@@ -116,6 +117,28 @@ GWAS_API gwas_status gwas_setup(const gwas_options* opt, int64_t n, int64_t p, i
                        const double* h2, const double* sigma2,
                        void* state_dev, size_t state_bytes, void* work_dev, size_t work_bytes,
                        gwas_ctx** out);
+
+/* The paper's first step ("the reduced model (with X = [1 | L]) is fit to the data, thus obtaining the
+ * estimates {sigma2^, h2^}"; eigen-based ML (GenABEL, FaST-LMM) or REML (EMMAX), cost 10/3 n^3 + O(v n p^2))
+ * followed by gwas_setup with those estimates, sharing one eigendecomposition.  After Alg. 4 lines 1, 2, 4 every
+ * trait's profile log-likelihood l_j(h) (beta and sigma2 profiled out; reading E1) is evaluated in the
+ * eigenbasis on the grid h = g/100, g = 0..100 (points with some h w_k + 1 - h <= eps_spd are infeasible), and
+ * the first grid maximum is refined by 50 bisection steps on the sign of dl/dh in the neighbouring grid interval
+ * (readings E2, E3).  sigma2_j = R/n (ML) or R/(n - p) (REML) at h2_j.  Requires opt->algorithm = GWAS_ALG_EIG.
+ *   method        GWAS_EST_ML or GWAS_EST_REML
+ *   h2_out, sigma2_out, loglik_out   t doubles each, host or device, may be NULL; written before returning
+ *   other arguments as gwas_setup (without h2 / sigma2).
+ * Errors: GWAS_E_ARG (bad method / algorithm), GWAS_E_NOT_SPD naming the first trait whose residual R is not > 0
+ * (y_j in the span of X_L) or that has no feasible grid point; otherwise as gwas_setup.  The estimation time
+ * (kernels only) is reported by gwas_estimate_ms. */
+GWAS_API gwas_status gwas_setup_estimate(const gwas_options* opt, int64_t n, int64_t p, int64_t t,
+                                const double* phi, const double* XL, const double* Y, int32_t method,
+                                double* h2_out, double* sigma2_out, double* loglik_out,
+                                void* state_dev, size_t state_bytes, void* work_dev, size_t work_bytes,
+                                gwas_ctx** out);
+
+/* Event time (ms) of the estimation kernels of gwas_setup_estimate (0 for a gwas_setup context). */
+GWAS_API gwas_status gwas_estimate_ms(gwas_ctx* ctx, double* ms);
 
 /* For ranks != 0 after state_dev was broadcast from a gwas_setup rank: validates the state header against
  * (n, p, t, opt) and creates a context.  Synchronises. */

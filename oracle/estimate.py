@@ -41,6 +41,7 @@ ML = 0
 REML = 1
 GRID = 100
 BISECT_ITERS = 50
+R_REL_MIN = 1e-24  # reading E1: R <= 1e-24 y^T V^-1 y (relative residual 1e-12) means y lies in span(X_L)
 
 
 def _chol(V):
@@ -50,7 +51,8 @@ def _chol(V):
 def profile_loglik(Phi, XL, y, h, method=ML, with_derivative=False):
     """Profile log-likelihood of the reduced model at h (definitions in the module docstring).
 
-    Returns dict(ll, sigma2, beta, R, dll (if with_derivative)).  Raises ValueError if V(h) is not SPD or R <= 0."""
+    Returns dict(ll, sigma2, beta, R, dll (if with_derivative)).  Raises ValueError if V(h) is not SPD or
+    R <= R_REL_MIN * y^T V^-1 y (y in the span of X_L)."""
     Phi = np.asarray(Phi, dtype=np.float64)
     X = np.asarray(XL, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
@@ -70,7 +72,7 @@ def profile_loglik(Phi, XL, y, h, method=ML, with_derivative=False):
     r = y - X @ beta
     rw = sla.solve_triangular(L, r, lower=True)
     R = float(rw @ rw)
-    if not (R > 0.0) or not np.isfinite(R):
+    if not (R > R_REL_MIN * float(yw @ yw)) or not np.isfinite(R):  # reading E1: exact fit is an error
         raise ValueError(f"residual R = {R} at h = {h}: y in the span of X_L")
     if method == ML:
         nn = n

@@ -16,9 +16,10 @@ VAR_TEXTBOOK, VAR_LITERAL = 0, 1
 PAIR_OK, PAIR_COLLINEAR, PAIR_NONFINITE = 0, 1, 2
 K1, K2, K3, H2D = 0, 1, 2, 3
 ALG_EIG, ALG_CHOL = 0, 1
+EST_ML, EST_REML = 0, 1
 NUM_TIMERS = 4
 
-EXPORTS = ["gwas_default_options", "gwas_state_bytes", "gwas_workspace_bytes", "gwas_setup", "gwas_attach",
+EXPORTS = ["gwas_default_options", "gwas_state_bytes", "gwas_workspace_bytes", "gwas_setup", "gwas_setup_estimate", "gwas_estimate_ms", "gwas_attach",
            "gwas_run", "gwas_timings", "gwas_kernel_times", "gwas_gemm_tn", "gwas_destroy", "gwas_last_error",
            "gwas_version"]
 
@@ -49,6 +50,8 @@ def _load():
         "gwas_state_bytes": (sz, [i64, i64, i64, opt]),
         "gwas_workspace_bytes": (sz, [i64, i64, i64, opt]),
         "gwas_setup": (C.c_int, [opt, i64, i64, i64, P, P, P, P, P, P, sz, P, sz, C.POINTER(P)]),
+        "gwas_setup_estimate": (C.c_int, [opt, i64, i64, i64, P, P, P, i32, P, P, P, P, sz, P, sz, C.POINTER(P)]),
+        "gwas_estimate_ms": (C.c_int, [P, dp]),
         "gwas_attach": (C.c_int, [opt, i64, i64, i64, P, sz, P, sz, C.POINTER(P)]),
         "gwas_run": (C.c_int, [P, i64, P, i64, P, P, P]),
         "gwas_timings": (C.c_int, [P, dp, dp, dp]),

@@ -22,6 +22,7 @@ _XR = {"u8": _lib.XR_U8, "f64": _lib.XR_F64}
 _OUT = {"snp": _lib.OUT_SNP, "full": _lib.OUT_FULL}
 _VAR = {"textbook": _lib.VAR_TEXTBOOK, "literal": _lib.VAR_LITERAL}
 _ALG = {"eig": _lib.ALG_EIG, "chol": _lib.ALG_CHOL}
+_EST = {"ml": _lib.EST_ML, "reml": _lib.EST_REML}
 
 
 def _ptr(x) -> int:
@@ -97,6 +98,31 @@ class Gwas:
                                  _ptr(ss), self.state.data_ptr(), self.state_bytes, self.work.data_ptr(),
                                  self.work_bytes, C.byref(self._ctx)))
         return self
+
+    def setup_estimate(self, Phi, XL, Y, method: str = "reml"):
+        """The paper's first step + setup: estimate (h2_j, sigma2_j) per trait by ML / REML in the
+        eigenbasis, then precompute with them.  Returns dict(h2, sigma2, loglik) as float64 numpy arrays (t,)."""
+        self._close_ctx()
+        phi = _colmajor_f64(Phi)
+        xl = _colmajor_f64(XL)
+        y = _colmajor_f64(np.asarray(Y).reshape(self.n, self.t) if not isinstance(Y, torch.Tensor) else Y.reshape(self.n, self.t))
+        for a, shape in ((phi, (self.n, self.n)), (xl, (self.n, self.p))):
+            if tuple(a.shape) != shape and tuple(a.shape)[::-1] != shape:
+                raise ValueError(f"bad input shape {tuple(a.shape)}, expected {shape}")
+        h2 = np.empty(self.t)
+        s2 = np.empty(self.t)
+        ll = np.empty(self.t)
+        with torch.cuda.device(self.device):
+            check(lib.gwas_setup_estimate(C.byref(self.opt), self.n, self.p, self.t, _ptr(phi), _ptr(xl), _ptr(y),
+                                          _EST[method], h2.ctypes.data, s2.ctypes.data, ll.ctypes.data,
+                                          self.state.data_ptr(), self.state_bytes, self.work.data_ptr(),
+                                          self.work_bytes, C.byref(self._ctx)))
+        return {"h2": h2, "sigma2": s2, "loglik": ll}
+
+    def estimate_ms(self) -> float:
+        ms = C.c_double()
+        check(lib.gwas_estimate_ms(self._ctx, C.byref(ms)))
+        return ms.value
 
     def attach(self):
         """Non-setup ranks: self.state was filled by a broadcast; validate it and create the context."""

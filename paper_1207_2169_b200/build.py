@@ -8,7 +8,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgwas.so")
 SOURCES = ["gwas.cu"]
-HEADERS = ["gemm_dmma.cuh", "gemm_i8.cuh", "schur.cuh", "setup_kernels.cuh"]
+HEADERS = ["estimate.cuh", "gemm_dmma.cuh", "gemm_i8.cuh", "schur.cuh", "setup_kernels.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

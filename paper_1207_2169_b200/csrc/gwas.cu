@@ -17,6 +17,7 @@
 
 #include "../../include/gwas.h"
 #include "gemm_dmma.cuh"
+#include "estimate.cuh"
 #include "gemm_i8.cuh"
 #include "schur.cuh"
 #include "setup_kernels.cuh"
@@ -174,7 +175,7 @@ RunLayout run_layout(const Dims& d, bool overlap) {
 }
 
 struct SetupLayout {
-  size_t xlpad, ypad, xlp, yp, stl, h2, s2, err, info, work, zt, blin, total;
+  size_t xlpad, ypad, xlp, yp, stl, h2, s2, err, info, est_rec, est_ll, est_gs, work, zt, blin, total;
 };
 SetupLayout setup_layout(const Dims& d, int64_t lwork) {
   SetupLayout s;
@@ -193,6 +194,9 @@ SetupLayout setup_layout(const Dims& d, int64_t lwork) {
   s.s2 = take(sizeof(double) * d.t);
   s.err = take(sizeof(unsigned long long) * 4);
   s.info = take(sizeof(int) * 4);
+  s.est_rec = take(sizeof(double) * (gw::EST_GRID + 1) * gw::est_rec((int)d.p));
+  s.est_ll = take(sizeof(double) * d.t);
+  s.est_gs = take(sizeof(int) * d.t);
   s.work = take(sizeof(double) * (size_t)std::max<int64_t>(lwork, 1));
   s.zt = s.blin = 0;
   if (d.i8) {  // Z^T and B_lin = Z B_op (reuse the dsyevd workspace region's tail: allocated after it)
@@ -487,6 +491,29 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   return GWAS_OK;
 }
 
+// Variance-component estimation kernels (estimate.cuh), dispatched on the compile-time p.
+template <int P>
+gwas_status launch_estimate_p(const double* W, const double* xlp, const double* yp, int n, int kpad, int t, int method,
+                              double eps_spd, double* rec, gw::EstOut eo, cudaStream_t st) {
+  gw::est_grid_shared<P><<<gw::EST_GRID + 1, gw::EST_THREADS, 0, st>>>(W, xlp, n, kpad, eps_spd, rec);
+  CKC(cudaGetLastError());
+  gw::est_traits<P><<<(unsigned)t, gw::EST_THREADS, 0, st>>>(W, xlp, yp, n, kpad, t, method, rec, eo);
+  CKC(cudaGetLastError());
+  return GWAS_OK;
+}
+
+gwas_status launch_estimate(int p, const double* W, const double* xlp, const double* yp, int n, int kpad, int t,
+                            int method, double eps_spd, double* rec, gw::EstOut eo, cudaStream_t st) {
+  switch (p) {
+#define EST_CASE(P) \
+  case P: return launch_estimate_p<P>(W, xlp, yp, n, kpad, t, method, eps_spd, rec, eo, st);
+    EST_CASE(1) EST_CASE(2) EST_CASE(3) EST_CASE(4) EST_CASE(5) EST_CASE(6)
+    EST_CASE(7) EST_CASE(8) EST_CASE(9) EST_CASE(10) EST_CASE(11) EST_CASE(12)
+#undef EST_CASE
+    default: return fail(GWAS_E_ARG, "estimation: p = %d unsupported", p);
+  }
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -524,7 +551,7 @@ struct gwas_ctx {
   cudaEvent_t ev_out_ready[2] = {nullptr, nullptr}, ev_out_free[2] = {nullptr, nullptr}, ev_djoin = nullptr;
   int stage_next = 0;
   bool stage_zeroed = false;
-  float ms_eig = 0.f, ms_pre = 0.f;
+  float ms_eig = 0.f, ms_pre = 0.f, ms_est = 0.f;
   // per-kernel event timers
   struct Pending {
     int kind;
@@ -653,12 +680,19 @@ size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options*
   return std::max(setup_layout(d, lwork).total, run_layout(d, o->overlap != 0).total);
 }
 
-gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, const double* phi, const double* XL,
-                       const double* Y, const double* h2, const double* sigma2, void* state_dev, size_t state_bytes,
-                       void* work_dev, size_t work_bytes, gwas_ctx** out) {
+}  // extern "C"
+
+namespace {
+// gwas_setup (est_method < 0: h2 / sigma2 given) and gwas_setup_estimate (est_method = GWAS_EST_ML / _REML: h2 and
+// sigma2 estimated in the eigenbasis after Alg. 4 lines 1, 2, 4, then the same per-trait precompute).
+gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, const double* phi, const double* XL,
+                       const double* Y, const double* h2, const double* sigma2, int est_method, double* h2_out,
+                       double* s2_out, double* ll_out, void* state_dev, size_t state_bytes, void* work_dev,
+                       size_t work_bytes, gwas_ctx** out) {
   g_err.clear();
   CKG(check_sizes(n, p, t, o));
-  if (!out || !phi || !XL || !Y || !h2 || !sigma2 || !state_dev || !work_dev)
+  const bool est = est_method >= 0;
+  if (!out || !phi || !XL || !Y || (!est && (!h2 || !sigma2)) || !state_dev || !work_dev)
     return fail(GWAS_E_ARG, "NULL pointer argument");
   *out = nullptr;
   CKC(cudaSetDevice(o->device));
@@ -676,8 +710,13 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
 
   // validate (h2, sigma2) on the host
   std::vector<double> hh(t), ss(t);
-  CKC(cudaMemcpy(hh.data(), h2, sizeof(double) * t, cudaMemcpyDefault));
-  CKC(cudaMemcpy(ss.data(), sigma2, sizeof(double) * t, cudaMemcpyDefault));
+  if (!est) {
+    CKC(cudaMemcpy(hh.data(), h2, sizeof(double) * t, cudaMemcpyDefault));
+    CKC(cudaMemcpy(ss.data(), sigma2, sizeof(double) * t, cudaMemcpyDefault));
+  } else {
+    std::fill(hh.begin(), hh.end(), 0.5);
+    std::fill(ss.begin(), ss.end(), 1.0);
+  }
   for (int64_t j = 0; j < t; ++j) {
     if (!(hh[j] >= 0.0 && hh[j] <= 1.0)) return fail(GWAS_E_ARG, "h2[%lld] = %g outside [0, 1]", (long long)j, hh[j]);
     if (!(ss[j] > 0.0) || !std::isfinite(ss[j])) return fail(GWAS_E_ARG, "sigma2[%lld] = %g not > 0", (long long)j, ss[j]);
@@ -715,9 +754,11 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     CKC(cudaMemsetAsync(c->W(), 0, sizeof(double) * d.kpad, cs));
     CKC(cudaMemcpy2DAsync(c->Z(), sizeof(double) * d.kpad, phi, sizeof(double) * n, sizeof(double) * n, n,
                           cudaMemcpyDefault, cs));
-    CKC(cudaMemcpyAsync(dh2, h2, sizeof(double) * t, cudaMemcpyDefault, cs));
-    CKC(cudaMemcpyAsync(ds2, sigma2, sizeof(double) * t, cudaMemcpyDefault, cs));
-    CKC(cudaMemcpyAsync(c->s2(), sigma2, sizeof(double) * t, cudaMemcpyDefault, cs));
+    if (!est) {
+      CKC(cudaMemcpyAsync(dh2, h2, sizeof(double) * t, cudaMemcpyDefault, cs));
+      CKC(cudaMemcpyAsync(ds2, sigma2, sizeof(double) * t, cudaMemcpyDefault, cs));
+      CKC(cudaMemcpyAsync(c->s2(), sigma2, sizeof(double) * t, cudaMemcpyDefault, cs));
+    }
     CKC(cudaMemcpy2DAsync(xlpad, sizeof(double) * d.kpad, XL, sizeof(double) * n, sizeof(double) * n, p,
                           cudaMemcpyDefault, cs));
     CKC(cudaMemcpy2DAsync(ypad, sizeof(double) * d.kpad, Y, sizeof(double) * n, sizeof(double) * n, t,
@@ -780,6 +821,19 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     // Alg. 4 lines 2, 4: X_L' = Z^T X_L, Y' = Z^T Y  (K1 kernel, fp64 A)
     CKG(gemm_tn(false, xlpad, d.kpad, c->Z(), d.kpad, xlp, d.kpad, p, n, n, n, cs));
     CKG(gemm_tn(false, ypad, d.kpad, c->Z(), d.kpad, yp, d.kpad, t, n, n, n, cs));
+    cudaEvent_t ee0 = nullptr, ee1 = nullptr;
+    if (est) {
+      // the paper's first step, eigen-based: per-trait (h2, sigma2) by ML / REML (readings E1-E4)
+      CKC(cudaEventCreate(&ee0));
+      CKC(cudaEventCreate(&ee1));
+      CKC(cudaEventRecord(ee0, cs));
+      gw::EstOut eo{dh2, ds2, reinterpret_cast<double*>(w + sl.est_ll), reinterpret_cast<int*>(w + sl.est_gs),
+                    derr + 2};
+      CKG(launch_estimate((int)p, c->W(), xlp, yp, (int)n, (int)d.kpad, (int)t, est_method, o->eps_spd,
+                          reinterpret_cast<double*>(w + sl.est_rec), eo, cs));
+      CKC(cudaMemcpyAsync(c->s2(), ds2, sizeof(double) * t, cudaMemcpyDeviceToDevice, cs));
+      CKC(cudaEventRecord(ee1, cs));
+    }
     // Alg. 4 lines 6, 8, 9: D_j and the D_j-scaled operand B2 = [B_op | D]
     {
       dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)d.n2);
@@ -811,9 +865,22 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
       CKC(cudaGetLastError());
     }
     CKC(cudaEventRecord(e3, cs));
-    unsigned long long herr[2];
+    unsigned long long herr[3];
     CKC(cudaMemcpyAsync(herr, derr, sizeof(herr), cudaMemcpyDeviceToHost, cs));
     CKC(cudaStreamSynchronize(cs));
+    if (est) {
+      float ms = 0.f;
+      CKC(cudaEventElapsedTime(&ms, ee0, ee1));
+      c->ms_est = ms;
+      cudaEventDestroy(ee0);
+      cudaEventDestroy(ee1);
+      if (herr[2] != ~0ull)
+        return fail(GWAS_E_NOT_SPD, "trait %lld: estimation failed (y_j in the span of X_L, or no feasible h2)",
+                    (long long)herr[2]);
+      if (h2_out) CKC(cudaMemcpy(h2_out, dh2, sizeof(double) * t, cudaMemcpyDefault));
+      if (s2_out) CKC(cudaMemcpy(s2_out, ds2, sizeof(double) * t, cudaMemcpyDefault));
+      if (ll_out) CKC(cudaMemcpy(ll_out, w + sl.est_ll, sizeof(double) * t, cudaMemcpyDefault));
+    }
     float ms_all = 0.f, ms_eig = 0.f;
     CKC(cudaEventElapsedTime(&ms_all, e0, e3));
     CKC(cudaEventElapsedTime(&ms_eig, e1, e2));
@@ -841,6 +908,38 @@ gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     return st;
   }
   *out = c;
+  return GWAS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+gwas_status gwas_setup(const gwas_options* o, int64_t n, int64_t p, int64_t t, const double* phi, const double* XL,
+                       const double* Y, const double* h2, const double* sigma2, void* state_dev, size_t state_bytes,
+                       void* work_dev, size_t work_bytes, gwas_ctx** out) {
+  return setup_impl(o, n, p, t, phi, XL, Y, h2, sigma2, -1, nullptr, nullptr, nullptr, state_dev, state_bytes,
+                    work_dev, work_bytes, out);
+}
+
+gwas_status gwas_setup_estimate(const gwas_options* o, int64_t n, int64_t p, int64_t t, const double* phi,
+                                const double* XL, const double* Y, int32_t method, double* h2_out, double* sigma2_out,
+                                double* loglik_out, void* state_dev, size_t state_bytes, void* work_dev,
+                                size_t work_bytes, gwas_ctx** out) {
+  g_err.clear();
+  if (!o) return fail(GWAS_E_ARG, "options is NULL");
+  if (method != GWAS_EST_ML && method != GWAS_EST_REML) return fail(GWAS_E_ARG, "bad estimation method %d", method);
+  if (o->algorithm != GWAS_ALG_EIG)
+    return fail(GWAS_E_ARG, "estimation runs in the eigenbasis: use GWAS_ALG_EIG (then pass the estimates to a "
+                            "GWAS_ALG_CHOL context's gwas_setup)");
+  if (method == GWAS_EST_REML && n <= p) return fail(GWAS_E_ARG, "REML needs n > p");
+  return setup_impl(o, n, p, t, phi, XL, Y, nullptr, nullptr, method, h2_out, sigma2_out, loglik_out, state_dev,
+                    state_bytes, work_dev, work_bytes, out);
+}
+
+gwas_status gwas_estimate_ms(gwas_ctx* c, double* ms) {
+  g_err.clear();
+  if (!c || !ms) return fail(GWAS_E_ARG, "NULL argument");
+  *ms = c->ms_est;
   return GWAS_OK;
 }
 

@@ -194,3 +194,13 @@ def test_consistency_on_simulated_traits():
     est = E.estimate(ds.Phi, ds.XL, ds.Y, E.REML, iters=30)
     assert abs(np.mean(est["h2"]) - 0.6) < 0.08
     assert abs(np.mean(est["sigma2"]) - 1.5) < 0.2
+
+
+def test_exact_fit_is_an_error():
+    """Reading E1: y in the span of X_L (R = 0 up to rounding) has no finite likelihood maximum -> ValueError."""
+    Phi, XL, _ = _problem(seed=2)
+    y = XL @ np.array([1.0, -2.0, 0.5])
+    with pytest.raises(ValueError):
+        E.profile_loglik(Phi, XL, y, 0.4, E.REML)
+    with pytest.raises(ValueError):
+        E.estimate_trait(Phi, XL, y, E.ML)
