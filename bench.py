@@ -368,6 +368,11 @@ def run_ours(args):
             engc.close()
             serc.close()
 
+    # ================= variance-component estimation (the paper's first step, NEXT-3) =================
+    est_mode = None
+    if args.est_alt and rank == 0:
+        est_mode = bench_estimate(gw, cfg, ds, local, args)
+
     # ---------------- parity spot check on this run's outputs (outside timed regions)
     parity = None
     if args.check and rank == 0:
@@ -410,9 +415,11 @@ def run_ours(args):
             "setup": {**setup, "datagen_s": t_gen},
             "clocks": clocks,
         }
-        if alt is not None or chol_modes:
+        if alt is not None or chol_modes or est_mode:
             res["modes"] = ({"int8_sliced": alt} if alt is not None else {})
             res["modes"].update(chol_modes)
+            if est_mode:
+                res["modes"]["estimate"] = est_mode
         if parity is not None:
             res["parity"] = parity
         if not args.no_cpu_baseline:
@@ -425,6 +432,40 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return res
+
+
+def est_passes(p):
+    """Streaming passes over (W, X_L', y'_j) per trait in est_traits (estimate.cuh): 26 grid passes (4 grid points
+    each), 2 per derivative evaluation (1 at the grid argmax + EST_ITERS bisection steps) and 2 for the final
+    evaluation."""
+    return 26 + 2 * (1 + 50) + 2
+
+
+def bench_estimate(gw, cfg, ds, local, args):
+    """gwas_setup_estimate on the config's traits (REML and ML): kernel time from CUDA events (gwas_estimate_ms),
+    traits/s, the bytes the kernels stream per trait (mostly L2 hits: X_L' and W are shared by all traits), and the
+    estimates against the simulated truth (reading A13).  Parity with the oracle is in tests/test_gpu_estimate.py."""
+    import torch
+    out = {}
+    for method in ("reml", "ml"):
+        eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=local, block_cols=args.block)
+        ms = []
+        for _ in range(2):
+            est = eng.setup_estimate(ds.Phi, ds.XL, ds.Y, method)
+            ms.append(eng.estimate_ms())
+        tm = eng.timings()
+        eng.close()
+        torch.cuda.synchronize()
+        k = min(ms)
+        streamed = est_passes(cfg.p) * (cfg.p + 2) * 8.0 * cfg.n * cfg.t
+        err = est["h2"] - ds.h2
+        out[method] = {"ms": k, "traits_per_s": cfg.t / (k / 1e3), "ms_eig": tm["ms_eig"],
+                       "frac_of_eig": k / tm["ms_eig"],
+                       "streamed_gb_per_s": streamed / (k / 1e3) / 1e9,
+                       "h2_mean_err_vs_truth": float(np.mean(err)), "h2_rmse_vs_truth": float(np.sqrt(np.mean(err ** 2))),
+                       "h2_corr_vs_truth": float(np.corrcoef(est["h2"], ds.h2)[0, 1]) if cfg.t > 2 else None,
+                       "sigma2_mean_ratio_vs_truth": float(np.mean(est["sigma2"] / ds.s2))}
+    return out
 
 
 def cpu_baseline_sample(cfg, ds, args):
@@ -510,6 +551,8 @@ def main(argv=None):
                     help="skip the CLAK-Chol (Alg. 3) modes reported under `modes` for single-trait configs")
     ap.add_argument("--no-int8-alt", dest="int8_alt", action="store_false",
                     help="skip the int8-sliced mode measurement reported under `modes`")
+    ap.add_argument("--no-est-alt", dest="est_alt", action="store_false",
+                    help="skip the variance-component estimation measurement reported under `modes.estimate`")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--check", type=int, default=2000, help="oracle spot-check pairs after timing (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
