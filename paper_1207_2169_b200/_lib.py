@@ -29,7 +29,7 @@ class GwasOptions(C.Structure):
                 ("var_convention", C.c_int32), ("block_cols", C.c_int64), ("eps_spd", C.c_double),
                 ("eps_collinear", C.c_double), ("compute_stream", C.c_void_p), ("copy_stream", C.c_void_p),
                 ("timing", C.c_int32), ("int8_slices", C.c_int32),
-                ("overlap", C.c_int32), ("algorithm", C.c_int32)]
+                ("overlap", C.c_int32), ("algorithm", C.c_int32), ("fuse_k2", C.c_int32)]
 
 
 class GwasError(RuntimeError):

@@ -47,7 +47,7 @@ class Gwas:
     def __init__(self, n: int, p: int, t: int, *, device: int = 0, xr_dtype: str = "u8", output_mode: str = "snp",
                  var_convention: str = "textbook", block_cols: int = 8192, timing: bool = False,
                  eps_spd: float = 1e-10, eps_collinear: float = 1e-10, compute_stream=None, copy_stream=None,
-                 int8_slices: int = 0, overlap: bool = False, algorithm: str = "eig"):
+                 int8_slices: int = 0, overlap: bool = False, algorithm: str = "eig", fuse_k2: bool = True):
         self.n, self.p, self.t = int(n), int(p), int(t)
         self.w = self.p + 1
         self.device = torch.device("cuda", device)
@@ -69,6 +69,7 @@ class Gwas:
         o.int8_slices = int(int8_slices)
         o.overlap = 1 if overlap else 0
         o.algorithm = _ALG[algorithm]
+        o.fuse_k2 = 1 if fuse_k2 else 0
         self.opt = o
         self.state_bytes = lib.gwas_state_bytes(self.n, self.p, self.t, C.byref(o))
         if self.state_bytes == 0:

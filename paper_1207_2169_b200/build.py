@@ -1,4 +1,8 @@
-"""Build libgwas.so in-tree with nvcc for sm_100a (explicit -gencode; no torch arch list involved)."""
+"""Build libgwas.so in-tree with nvcc for sm_100a (explicit -gencode; no torch arch list involved).
+
+Each translation unit under csrc/ is compiled to an object in parallel (the estimation kernels are instantiated
+for p = 1..12 across four units), then nvcc links the shared library against cuSOLVER."""
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
@@ -7,12 +11,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgwas.so")
-SOURCES = ["gwas.cu"]
-HEADERS = ["estimate.cuh", "gemm_dmma.cuh", "gemm_i8.cuh", "schur.cuh", "setup_kernels.cuh"]
+OBJ_DIR = os.path.join(HERE, "build")
+SOURCES = ["gwas.cu", "est_p1_3.cu", "est_p4_6.cu", "est_p7_9.cu", "est_p10_12.cu"]
+HEADERS = ["estimate.cuh", "estimate_launch.cuh", "gemm_dmma.cuh", "gemm_i8.cuh", "schur.cuh", "setup_kernels.cuh"]
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMPILE_FLAGS = ARCH + [
+    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr", "-Xptxas", "-v",
 ]
 
@@ -30,22 +35,37 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
+def _compile(src):
+    obj = os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
+    cmd = [_nvcc(), *COMPILE_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return src, obj, r
+
+
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(_compile, SOURCES))
+    info = []
+    for src, obj, r in results:
+        info.append(f"==== {src}\n{r.stderr}")
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed compiling {src}")
     cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp",
+    cmd = [_nvcc(), *ARCH, "-shared", *[obj for _, obj, _ in results], "-o", LIB + ".tmp",
            "-L", os.path.join(cuda, "lib64"), "-lcusolver", "-Xlinker", "-rpath=" + os.path.join(cuda, "lib64")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libgwas.so")
+        raise RuntimeError("nvcc failed linking libgwas.so")
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write("".join(info))
     os.replace(LIB + ".tmp", LIB)
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+        f.write("".join(info))
     return LIB
 
 

@@ -37,7 +37,29 @@ struct GemmShape {
   long long split_stride;
   int tri;        // B lower-triangular in (row, k): row c has no entries at k > c (CLAK-Chol's L^-1), so an output
                   // tile [n0, n0 + BN) only needs k < n0 + BN
+  // K2 fused into K1's epilogue (few traits; template FUSE): instead of storing the tile of
+  // C = X_R'^T, each CTA contracts it with the fnq K2 operand rows it covers and stores the per-tile partial sums
+  // P[tn][i][qq] = sum_{c in tile tn} X_R'[c, i]^e B2[row(qq), c], e = 1 for qq < fnlin (row qq), e = 2 otherwise
+  // (row fnsq + qq - fnlin); fused_k2_reduce sums them over tn in fixed order.
+  const double* fB;
+  long long fldb;
+  int fnq, fnlin, fnsq;
+  double* fP;
+  long long fP_stride;  // doubles per tn
 };
+
+constexpr int FUSE_MAX_NQ = 32;  // fused K2 columns t (p + 2) per CTA (fits the freed stage buffers)
+
+// C[i][col(qq)] = sum_tn P[tn][i][qq], col(qq) = qq (qq < nlin) or nsq + qq - nlin: the fused K2 finished in fixed order.
+__global__ void fused_k2_reduce(const double* __restrict__ P, long long stride, int ntiles, int M, int nq, int nlin,
+                                int nsq, double* __restrict__ C, long long ldc) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)M * nq) return;
+  const int i = (int)(idx / nq), qq = (int)(idx - (long long)i * nq);
+  double acc = P[idx];
+  for (int tn = 1; tn < ntiles; ++tn) acc += P[tn * stride + idx];
+  C[(long long)i * ldc + (qq < nlin ? qq : nsq + qq - nlin)] = acc;
+}
 
 // Fixed-order sum of the split-K partial products: C[i][c] = sum_s P_s[i][c] (deterministic, independent of M).
 __global__ void splitk_reduce(const double* __restrict__ P, long long split_stride, int ksplit, int M, int N,
@@ -147,7 +169,7 @@ __device__ __forceinline__ double load_a<double>(const uint8_t* a_tile, const do
 }
 
 // One CTA computes a BM x BN tile of C with 8 warps (warp grid 2 x 4 for 128 x 128); thread 0 also issues TMA.
-template <typename TA, int BM, int BN, int STAGES, bool SQ>
+template <typename TA, int BM, int BN, int STAGES, bool SQ, bool FUSE = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tn_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape s) {
   constexpr int WARPS_N = BN / 32;  // warp tiles are always 32 columns wide (K2's squaring is per warp)
@@ -302,19 +324,61 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   else
     mainloop(std::false_type{});
 
-  // ---------------- epilogue: each lane owns C[row][2q, 2q+1] of every 8x8 fragment
+  if constexpr (FUSE) {
+    // ---------------- fused K2 epilogue: per-tile partial contractions with the K2 operand rows
+    __syncthreads();  // every warp is done with the stage buffers: reuse them for the cross-warp reduction
+    double* red = reinterpret_cast<double*>(smem);  // [WARPS_N][BM][fnq]
+    const int nq = s.fnq;
+    for (int qq = 0; qq < nq; ++qq) {
+      const bool sqc = qq >= s.fnlin;
+      const double* brow = s.fB + (long long)(sqc ? s.fnsq + (qq - s.fnlin) : qq) * s.fldb;
+      double bv[NI][2];
 #pragma unroll
-  for (int i = 0; i < MI; ++i) {
-    const int row = m0 + wm * WM + i * 8 + g;
-    if (row >= s.M) continue;
-    double* crow = s.C + split * s.split_stride + (long long)row * s.ldc;
+      for (int j = 0; j < NI; ++j) {
+        const int col = n0 + wn * WN + j * 8 + 2 * q;
+        bv[j][0] = col < s.N ? __ldg(brow + col) : 0.0;
+        bv[j][1] = col + 1 < s.N ? __ldg(brow + col + 1) : 0.0;
+      }
 #pragma unroll
-    for (int j = 0; j < NI; ++j) {
-      const int col = n0 + wn * WN + j * 8 + 2 * q;
-      if (col + 1 < s.N) {
-        *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
-      } else if (col < s.N) {
-        crow[col] = acc[i][j][0];
+      for (int i = 0; i < MI; ++i) {
+        double sum = 0.0;
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const double a0 = sqc ? acc[i][j][0] * acc[i][j][0] : acc[i][j][0];
+          const double a1 = sqc ? acc[i][j][1] * acc[i][j][1] : acc[i][j][1];
+          sum = fma(a0, bv[j][0], sum);
+          sum = fma(a1, bv[j][1], sum);
+        }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (q == 0) red[((long long)wn * BM + wm * WM + i * 8 + g) * nq + qq] = sum;
+      }
+    }
+    __syncthreads();
+    double* P = s.fP + (long long)tn * s.fP_stride;
+    for (int idx = threadIdx.x; idx < BM * nq; idx += GEMM_THREADS) {
+      const int r = idx / nq;
+      if (m0 + r >= s.M) continue;
+      double v = red[idx];
+#pragma unroll
+      for (int w2 = 1; w2 < WARPS_N; ++w2) v += red[(long long)w2 * BM * nq + idx];
+      P[(long long)(m0 + r) * nq + (idx - r * nq)] = v;
+    }
+  } else {
+    // ---------------- epilogue: each lane owns C[row][2q, 2q+1] of every 8x8 fragment
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int row = m0 + wm * WM + i * 8 + g;
+      if (row >= s.M) continue;
+      double* crow = s.C + split * s.split_stride + (long long)row * s.ldc;
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int col = n0 + wn * WN + j * 8 + 2 * q;
+        if (col + 1 < s.N) {
+          *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else if (col < s.N) {
+          crow[col] = acc[i][j][0];
+        }
       }
     }
   }

@@ -50,7 +50,16 @@ struct I8Shape {
   const int* exps;    // 2^e per output column of the concatenated digit matrix (tiles*64 entries)
   int group_m;
   int tri_tiles;      // output tiles [0, tri_tiles) come from a lower-triangular B (CLAK-Chol's L^-1): K < (tn+1)*64
+  // K2b fused into the epilogue (ft <= I8_FUSE_T traits; ft = 0: off): the C_a tiles are not
+  // stored; each thread accumulates P[tn][row][j] = sum_{c in tile} X_R'[c, row]^2 d_j[c] (d_j = row j of fD, ld fld)
+  // for its row, and fused_k2_reduce sums the partials over the C_a tiles in fixed order.
+  int ft;
+  const double* fD;
+  long long fld;
+  double* fP;
+  long long fP_stride;
 };
+constexpr int I8_FUSE_T = 8;
 
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
   // K-major, 64-byte swizzle: 8-row atoms of 64 B (SBO = 512 B between atoms), LBO unused (encoded 1),
@@ -130,6 +139,11 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
   const int oc0 = tn * I8_NB;  // first output column of the concatenated digit matrix
+  const bool in_a = tn < s.na_tiles;
+  const bool fuse = in_a && s.ft > 0;
+  double part[I8_FUSE_T];
+#pragma unroll
+  for (int jj = 0; jj < I8_FUSE_T; ++jj) part[jj] = 0.0;
 #pragma unroll 1
   for (int j0 = 0; j0 < I8_NB; j0 += 16) {
     double acc[16];
@@ -145,8 +159,19 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
 #pragma unroll
       for (int c = 0; c < 16; ++c) acc[c] = fma(acc[c], 0.0078125, (double)v[c]);  // acc * 2^-7 + I_s
     }
-    if (row < s.M) {
-      const bool in_a = tn < s.na_tiles;
+    if (fuse) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int col = oc0 + j0 + c;
+        if (col < s.na) {
+          const double x = scalbn(acc[c], __ldg(s.exps + col) - 7);
+          const double x2 = x * x;
+#pragma unroll
+          for (int jj = 0; jj < I8_FUSE_T; ++jj)
+            if (jj < s.ft) part[jj] = fma(x2, __ldg(s.fD + jj * s.fld + col), part[jj]);
+        }
+      }
+    } else if (row < s.M) {
       double* crow = in_a ? s.Ca + (long long)row * s.lda_c : s.Cb + (long long)row * s.ldb_c;
       const int cbase = in_a ? oc0 + j0 : (tn - s.na_tiles) * I8_NB + j0;
       const int cmax = in_a ? s.na : s.nb;
@@ -163,7 +188,12 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
       }
     }
   }
-
+  if (fuse && row < s.M) {
+    double* P = s.fP + (long long)tn * s.fP_stride + (long long)row * s.ft;
+#pragma unroll
+    for (int jj = 0; jj < I8_FUSE_T; ++jj)
+      if (jj < s.ft) P[jj] = part[jj];
+  }
 }
 
 // CL = cluster size along M: the CL CTAs of a cluster compute CL consecutive row tiles of the same output

@@ -17,7 +17,7 @@
 
 #include "../../include/gwas.h"
 #include "gemm_dmma.cuh"
-#include "estimate.cuh"
+#include "estimate_launch.cuh"
 #include "gemm_i8.cuh"
 #include "schur.cuh"
 #include "setup_kernels.cuh"
@@ -81,6 +81,8 @@ struct Dims {
   int64_t per_pair;                // outputs per pair: 1 (SNP mode) or p + 1 (full mode)
   int i8;                          // int8-sliced mode
   int64_t na_pad, nlin, nlin_pad;  // digit-matrix column blocks (multiples of 64)
+  bool fuse;                       // K2 fused into K1's epilogue (few traits, opt.fuse_k2)
+  int64_t fnq, ftiles;             // fused K2 columns per pair-row; max K1 column tiles (partials per block)
 };
 
 Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
@@ -100,6 +102,11 @@ Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   d.na_pad = round_up(n, gw::I8_NB);
   d.nlin = t * (p + 1);
   d.nlin_pad = round_up(d.nlin, gw::I8_NB);
+  // NEXT-2 fusion: FP64 mode contracts all t (p + 2) K2 columns in K1's epilogue, the int8 mode only the t squared
+  // columns (its linear K2 terms already come out of K1i)
+  d.fnq = d.i8 ? t : t * (p + 2);
+  d.fuse = o->fuse_k2 != 0 && (d.i8 ? t <= gw::I8_FUSE_T : d.fnq <= gw::FUSE_MAX_NQ);
+  d.ftiles = d.i8 ? d.na_pad / gw::I8_NB : (n + 63) / 64;
   return d;
 }
 
@@ -146,7 +153,7 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
 }
 
 struct RunLayout {
-  size_t stage[2], xrp[2], c2[2], split[2], outb[2], total;
+  size_t stage[2], xrp[2], c2[2], split[2], outb[2], fp[2], total;
   size_t out_bytes;  // per staging set: b, var (8 * per_pair each) + status (1) per pair of a block
 };
 // overlap mode double-buffers the rotated block and the K2 output so block b+1's K1 can run beside block b's K2/K3
@@ -170,6 +177,11 @@ RunLayout run_layout(const Dims& d, bool overlap) {
   r.out_bytes = (size_t)d.kb * d.t * (16 * d.per_pair + 1);
   r.outb[0] = take(r.out_bytes);
   r.outb[1] = take(r.out_bytes);
+  r.fp[0] = r.fp[1] = 0;
+  if (d.fuse) {  // per-tile partial sums of the fused K2
+    r.fp[0] = take(sizeof(double) * d.ftiles * d.kb * d.fnq);
+    r.fp[1] = overlap ? take(sizeof(double) * d.ftiles * d.kb * d.fnq) : r.fp[0];
+  }
   r.total = off;
   return r;
 }
@@ -303,11 +315,14 @@ constexpr size_t gemm_smem_bytes() {
   return 1024 + STAGES * (L::kAStride + L::kBStride) + 2 * STAGES * sizeof(uint64_t) + 256 * sizeof(double);
 }
 
-template <typename TA, int BN, int STAGES, bool SQ>
+template <typename TA, int BN, int STAGES, bool SQ, bool FUSE = false>
 gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw::GemmShape& s, cudaStream_t st) {
   static bool attr_set = false;  // per instantiation (the library binds one device per process)
   constexpr size_t smem = gemm_smem_bytes<TA, BN, STAGES>();
-  auto kern = gw::gemm_tn_dmma<TA, kBM, BN, STAGES, SQ>;
+  static_assert(!FUSE || (size_t)(BN / 32) * kBM * gw::FUSE_MAX_NQ * 8 <=
+                             (size_t)STAGES * (gw::GemmSmem<TA, kBM, BN>::kAStride + gw::GemmSmem<TA, kBM, BN>::kBStride),
+                "fused-K2 reduction buffer must fit in the stage buffers");
+  auto kern = gw::gemm_tn_dmma<TA, kBM, BN, STAGES, SQ, FUSE>;
   if (!attr_set) {
     CKC(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
@@ -325,9 +340,11 @@ gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw
 // are split along K into fixed ranges (independent of M, so results stay bitwise invariant to the block size)
 // and summed in fixed order.
 constexpr int kSplitMax = 8, kSplitLd = 64;
+// fuse (optional): K2 fused into the epilogue (GemmShape's f* fields; C is then not written, see gemm_dmma.cuh).
 gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                     int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st, int group_m = 16,
-                    double* split_scratch = nullptr, bool tri = false) {
+                    double* split_scratch = nullptr, bool tri = false, const gw::GemmShape* fuse = nullptr,
+                    int* tiles_n_out = nullptr) {
   if (M <= 0 || N <= 0) return GWAS_OK;
   if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
   if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
@@ -353,15 +370,31 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.nsq = (int)std::min<int64_t>(nsq, N);
   s.tiles_m = (int)((M + kBM - 1) / kBM);
   s.tiles_n = (int)((N + bn - 1) / bn);
+  if (tiles_n_out) *tiles_n_out = s.tiles_n;
   s.group_m = std::max(1, group_m);
   const int kt_all = (int)((K + gw::GEMM_BK - 1) / gw::GEMM_BK);
   s.ksplit = 1;
   s.kt_per_split = kt_all;
   s.split_stride = 0;
   s.tri = tri ? 1 : 0;
+  s.fB = nullptr;
+  s.fldb = 0;
+  s.fnq = s.fnlin = s.fnsq = 0;
+  s.fP = nullptr;
+  s.fP_stride = 0;
+  if (fuse) {
+    if (nsq < N || fuse->fnq > gw::FUSE_MAX_NQ || fuse->fnq < 1) return fail(GWAS_E_ARG, "bad fused-K2 shape");
+    s.fB = fuse->fB;
+    s.fldb = fuse->fldb;
+    s.fnq = fuse->fnq;
+    s.fnlin = fuse->fnlin;
+    s.fnsq = fuse->fnsq;
+    s.fP = fuse->fP;
+    s.fP_stride = fuse->fP_stride;
+  }
   double* c_final = C;
   int64_t ldc_final = ldc;
-  if (split_scratch && N <= kSplitLd && kt_all >= 16) {
+  if (split_scratch && !fuse && N <= kSplitLd && kt_all >= 16) {
     s.kt_per_split = std::max(8, (kt_all + kSplitMax - 1) / kSplitMax);
     s.ksplit = (kt_all + s.kt_per_split - 1) / s.kt_per_split;
     s.C = split_scratch;
@@ -371,6 +404,14 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   const bool sq = nsq < N;
   if (sq && (nsq % 32)) return fail(GWAS_E_ARG, "nsq must be a multiple of 32");
   auto launch = [&]() -> gwas_status {
+    if (fuse) {
+      if (bn == 64) {
+        if (a_u8) return launch_gemm_t<uint8_t, 64, kStagesU8, false, true>(ma, mb, s, st);
+        return launch_gemm_t<double, 64, kStagesF64N64, false, true>(ma, mb, s, st);
+      }
+      if (a_u8) return launch_gemm_t<uint8_t, 128, kStagesU8, false, true>(ma, mb, s, st);
+      return launch_gemm_t<double, 128, kStagesF64, false, true>(ma, mb, s, st);
+    }
     if (bn == 64) {
       if (a_u8) {
         if (sq) return launch_gemm_t<uint8_t, 64, kStagesU8, true>(ma, mb, s, st);
@@ -422,7 +463,9 @@ gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
 // K1i/K2a: C_a[i][c] (c < na) and C_b[i][c'] (c' < nb) from the u8 A block and the stacked digit matrix.
 gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const int8_t* dig, int64_t ldd,
                       int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
-                      double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st, int64_t tri_tiles = 0) {
+                      double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st, int64_t tri_tiles = 0,
+                      int ft = 0, const double* fD = nullptr, int64_t fld = 0, double* fP = nullptr,
+                      int64_t fP_stride = 0) {
   if (M <= 0) return GWAS_OK;
   // GWAS_I8_KERNEL: "1sm" (default) with GWAS_I8_CLUSTER (1, 2 or 4; default 2) CTAs multicasting the digit
   // slab, or "2sm" (CTA pairs with cta_group::2 MMAs).  Measured at C4 per 8192-column block: 1sm x1 14.4 ms,
@@ -457,6 +500,12 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   s.exps = exps;
   s.group_m = 64;
   s.tri_tiles = (int)tri_tiles;
+  if (ft < 0 || ft > gw::I8_FUSE_T) return fail(GWAS_E_ARG, "bad fused-K2b trait count");
+  s.ft = ft;
+  s.fD = fD;
+  s.fld = fld;
+  s.fP = fP;
+  s.fP_stride = fP_stride;
   constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256;
   constexpr size_t smem2 = 1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256;
   static bool attr_set = false;
@@ -491,27 +540,13 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   return GWAS_OK;
 }
 
-// Variance-component estimation kernels (estimate.cuh), dispatched on the compile-time p.
-template <int P>
-gwas_status launch_estimate_p(const double* W, const double* xlp, const double* yp, int n, int kpad, int t, int method,
-                              double eps_spd, double* rec, gw::EstOut eo, cudaStream_t st) {
-  gw::est_grid_shared<P><<<gw::EST_GRID + 1, gw::EST_THREADS, 0, st>>>(W, xlp, n, kpad, eps_spd, rec);
-  CKC(cudaGetLastError());
-  gw::est_traits<P><<<(unsigned)t, gw::EST_THREADS, 0, st>>>(W, xlp, yp, n, kpad, t, method, rec, eo);
-  CKC(cudaGetLastError());
-  return GWAS_OK;
-}
-
+// Variance-component estimation kernels (estimate.cuh), dispatched on the compile-time p (est_p*.cu).
 gwas_status launch_estimate(int p, const double* W, const double* xlp, const double* yp, int n, int kpad, int t,
                             int method, double eps_spd, double* rec, gw::EstOut eo, cudaStream_t st) {
-  switch (p) {
-#define EST_CASE(P) \
-  case P: return launch_estimate_p<P>(W, xlp, yp, n, kpad, t, method, eps_spd, rec, eo, st);
-    EST_CASE(1) EST_CASE(2) EST_CASE(3) EST_CASE(4) EST_CASE(5) EST_CASE(6)
-    EST_CASE(7) EST_CASE(8) EST_CASE(9) EST_CASE(10) EST_CASE(11) EST_CASE(12)
-#undef EST_CASE
-    default: return fail(GWAS_E_ARG, "estimation: p = %d unsupported", p);
-  }
+  if (p < 1 || p > 12) return fail(GWAS_E_ARG, "estimation: p = %d unsupported", p);
+  auto f = p <= 3 ? gw::est_launch_p1_3 : p <= 6 ? gw::est_launch_p4_6 : p <= 9 ? gw::est_launch_p7_9 : gw::est_launch_p10_12;
+  CKC(f(p, W, xlp, yp, n, kpad, t, method, eps_spd, rec, eo, st));
+  return GWAS_OK;
 }
 
 bool is_device_ptr(const void* p) {
@@ -660,6 +695,7 @@ void gwas_default_options(gwas_options* o) {
   o->compute_stream = nullptr;
   o->copy_stream = nullptr;
   o->timing = 0;
+  o->fuse_k2 = 1;
 }
 
 const char* gwas_last_error(void) { return g_err.c_str(); }
@@ -1032,10 +1068,24 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       A = stage;
       lda = d.kpad;
     }
+    double* fpart = d.fuse ? reinterpret_cast<double*>(c->work + c->rl.fp[set]) : nullptr;
+    const int64_t fstride = d.kb * d.fnq;
     if (!d.i8) {
       // K1 (Alg. 4 line 3): X_R'^T = X_R^T Z  (row i of xrp = Z^T g_i)
+      gw::GemmShape fz{};
+      int k1_tiles = 0;
+      if (d.fuse) {  // NEXT-2: K2 contracted in K1's epilogue, per column tile; X_R' never leaves the SM
+        fz.fB = c->B2();
+        fz.fldb = d.kpad;
+        fz.fnq = (int)d.fnq;
+        fz.fnlin = (int)(d.t * (d.p + 1));
+        fz.fnsq = (int)d.nsq;
+        fz.fP = fpart;
+        fz.fP_stride = fstride;
+      }
       CKG(c->tic(GWAS_K1, cs, &dummy));
-      CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64, nullptr, chol));
+      CKG(gemm_tn(u8, A, lda, c->Z(), d.kpad, xrp, d.kpad, cols, d.n, d.n, d.n, cs, 64, nullptr, chol,
+                  d.fuse ? &fz : nullptr, &k1_tiles));
       CKG(c->toc(cs));
       if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
       if (ovl) {
@@ -1044,13 +1094,21 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       }
       // K2 (Alg. 4 lines 13-15): all traits' W_R^T W_L, W_R^T y_j, W_R^T W_R in one product
       CKG(c->tic(GWAS_K2, cs2, &dummy));
-      CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, 16, splitbuf));
+      if (d.fuse) {
+        const long long tot = cols * d.fnq;
+        gw::fused_k2_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, cs2>>>(
+            fpart, fstride, k1_tiles, (int)cols, (int)d.fnq, (int)(d.t * (d.p + 1)), (int)d.nsq, c2, d.ldc2);
+        CKC(cudaGetLastError());
+      } else {
+        CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, 16, splitbuf));
+      }
       CKG(c->toc(cs2));
     } else {
       // K1i + K2a (int8-sliced, exact): X_R'^T = X_R^T Z and C[:, 0:t(p+1)] = X_R^T (Z B_op) in one launch
       CKG(c->tic(GWAS_K1, cs, &dummy));
       CKG(launch_i8(A, lda, cols, d.n, c->dig(), d.kpad, (d.na_pad + d.nlin_pad) / gw::I8_NB, d.na_pad / gw::I8_NB,
-                    c->exps(), xrp, d.kpad, d.n, c2, d.ldc2, d.nlin, cs, chol ? d.na_pad / gw::I8_NB : 0));
+                    c->exps(), xrp, d.kpad, d.n, c2, d.ldc2, d.nlin, cs, chol ? d.na_pad / gw::I8_NB : 0,
+                    d.fuse ? (int)d.t : 0, c->B2() + d.nsq * d.kpad, d.kpad, fpart, fstride));
       CKG(c->toc(cs));
       if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
       if (ovl) {
@@ -1059,8 +1117,15 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       }
       // K2b (DMMA): C[:, nsq + j] = sum_k X_R'[k,i]^2 d_j[k]  (W_R^T W_R, the term that needs the rotation)
       CKG(c->tic(GWAS_K2, cs2, &dummy));
-      CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, 0, cs2,
-                  16, splitbuf));
+      if (d.fuse) {  // NEXT-2: the squared term was contracted in K1i's epilogue; finish it in fixed order
+        const long long tot = cols * d.t;
+        gw::fused_k2_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, cs2>>>(
+            fpart, fstride, (int)(d.na_pad / gw::I8_NB), (int)cols, (int)d.t, 0, (int)d.nsq, c2, d.ldc2);
+        CKC(cudaGetLastError());
+      } else {
+        CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, 0, cs2,
+                    16, splitbuf));
+      }
       CKG(c->toc(cs2));
     }
     // K3 (Alg. 4 line 16): b_ij := S^-1 b_ij by Schur complement
