@@ -236,7 +236,7 @@ def run_ours(args):
     def make_engine(i8, overlap, algorithm="eig"):
         """Rank 0 sets up (eig + precompute), the state is replicated by ONE broadcast, other ranks attach."""
         eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=overlap,
-                      algorithm=algorithm)
+                      algorithm=algorithm, fuse_k2=bool(args.fuse_k2))
         info = {}
         if rank == 0:
             eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
@@ -254,7 +254,7 @@ def run_ours(args):
                 eng.attach()
         # a second, serial context on the same state (gwas_attach) times the kernels one by one
         ser = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=False,
-                      algorithm=algorithm)
+                      algorithm=algorithm, fuse_k2=bool(args.fuse_k2))
         ser.state.copy_(eng.state)
         ser.attach()
         return eng, ser, info
@@ -546,6 +546,7 @@ def main(argv=None):
     ap.add_argument("--block", type=int, default=8192, help="SNP columns per streamed block (k)")
     ap.add_argument("--snps", type=int, default=None, help="override m per rank (testing only)")
     ap.add_argument("--overlap", type=int, default=1, help="1: pipeline block b's K2/K3 beside block b+1's K1")
+    ap.add_argument("--fuse-k2", type=int, default=1, help="1: K2 fused into K1's epilogue for few traits (NEXT-2)")
     ap.add_argument("--kernel-steps", type=int, default=1, help="serial passes timed per kernel (roofline)")
     ap.add_argument("--no-chol-alt", dest="chol_alt", action="store_false",
                     help="skip the CLAK-Chol (Alg. 3) modes reported under `modes` for single-trait configs")

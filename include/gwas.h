@@ -90,7 +90,7 @@ typedef struct {
                               M = sigma2 (h2 Phi + (1 - h2) I) = L L^T (cuSOLVER dpotrf) and L^-1 (dtrtri) replace
                               the eigendecomposition; K1 becomes X_R := L^-1 X_R on the lower triangle only
                               (half the flops of Z^T X_R), K2/K3 run with D = I.  Fixed at setup (state). */
-  int32_t fuse_k2;         /* 1 (default): for few traits (FP64 mode t (p + 2) <= 32; int8-sliced mode t <= 8) K2 is
+  int32_t fuse_k2;         /* 1 (default): for few traits (FP64 mode t (p + 2) <= 28; int8-sliced mode t <= 8) K2 is
                               contracted inside K1's epilogue per column tile, so X_R' never
                               goes to HBM; a fixed-order reduction finishes it.  0: separate K2 product.  A run-time
                               choice (not part of the state); results differ from the unfused path only by rounding. */

@@ -4,14 +4,15 @@ Each translation unit under csrc/ is compiled to an object in parallel (the esti
 for p = 1..12 across four units), then nvcc links the shared library against cuSOLVER."""
 import concurrent.futures as cf
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgwas.so")
-OBJ_DIR = os.path.join(HERE, "build")
 SOURCES = ["gwas.cu", "est_p1_3.cu", "est_p4_6.cu", "est_p7_9.cu", "est_p10_12.cu"]
 HEADERS = ["estimate.cuh", "estimate_launch.cuh", "gemm_dmma.cuh", "gemm_i8.cuh", "schur.cuh", "setup_kernels.cuh"]
 
@@ -35,8 +36,8 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def _compile(src):
-    obj = os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
+def _compile(src, obj_dir):
+    obj = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
     cmd = [_nvcc(), *COMPILE_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return src, obj, r
@@ -45,9 +46,16 @@ def _compile(src):
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
-    os.makedirs(OBJ_DIR, exist_ok=True)
+    obj_dir = tempfile.mkdtemp(prefix="gwas_build_")  # objects stay out of the tree (they would travel to the box)
+    try:
+        return _build(obj_dir, verbose)
+    finally:
+        shutil.rmtree(obj_dir, ignore_errors=True)
+
+
+def _build(obj_dir, verbose):
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
-        results = list(ex.map(_compile, SOURCES))
+        results = list(ex.map(lambda src: _compile(src, obj_dir), SOURCES))
     info = []
     for src, obj, r in results:
         info.append(f"==== {src}\n{r.stderr}")

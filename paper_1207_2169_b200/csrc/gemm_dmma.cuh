@@ -48,7 +48,7 @@ struct GemmShape {
   long long fP_stride;  // doubles per tn
 };
 
-constexpr int FUSE_MAX_NQ = 32;  // fused K2 columns t (p + 2) per CTA (fits the freed stage buffers)
+constexpr int FUSE_MAX_NQ = 28;  // fused K2 columns t (p + 2) per CTA: reduction buffer + operand slice fit the freed stages
 
 // C[i][col(qq)] = sum_tn P[tn][i][qq], col(qq) = qq (qq < nlin) or nsq + qq - nlin: the fused K2 finished in fixed order.
 __global__ void fused_k2_reduce(const double* __restrict__ P, long long stride, int ntiles, int M, int nq, int nlin,
@@ -169,8 +169,9 @@ __device__ __forceinline__ double load_a<double>(const uint8_t* a_tile, const do
 }
 
 // One CTA computes a BM x BN tile of C with 8 warps (warp grid 2 x 4 for 128 x 128); thread 0 also issues TMA.
+// 64-wide tiles fit two CTAs per SM (smem and <= 128 registers): keep the fused variant there too.
 template <typename TA, int BM, int BN, int STAGES, bool SQ, bool FUSE = false>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, BN == 64 ? 2 : 1)
     gemm_tn_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape s) {
   constexpr int WARPS_N = BN / 32;  // warp tiles are always 32 columns wide (K2's squaring is per warp)
   constexpr int WARPS_M = GEMM_CONSUMER_WARPS / WARPS_N;
@@ -327,17 +328,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if constexpr (FUSE) {
     // ---------------- fused K2 epilogue: per-tile partial contractions with the K2 operand rows
     __syncthreads();  // every warp is done with the stage buffers: reuse them for the cross-warp reduction
-    double* red = reinterpret_cast<double*>(smem);  // [WARPS_N][BM][fnq]
     const int nq = s.fnq;
+    double* red = reinterpret_cast<double*>(smem);  // [WARPS_N][BM][fnq]
+    double* bsl = red + WARPS_N * BM * nq;          // [fnq][BN]: the tile's slice of the K2 operand rows
+    // one cooperative, coalesced load of the slice (a single L2 round trip instead of one per column)
+    for (int idx = threadIdx.x; idx < nq * BN; idx += GEMM_THREADS) {
+      const int qq = idx / BN, col = n0 + (idx - qq * BN);
+      const int brow = qq < s.fnlin ? qq : s.fnsq + (qq - s.fnlin);
+      bsl[idx] = col < s.N ? __ldg(s.fB + (long long)brow * s.fldb + col) : 0.0;
+    }
+    __syncthreads();
     for (int qq = 0; qq < nq; ++qq) {
       const bool sqc = qq >= s.fnlin;
-      const double* brow = s.fB + (long long)(sqc ? s.fnsq + (qq - s.fnlin) : qq) * s.fldb;
       double bv[NI][2];
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
-        const int col = n0 + wn * WN + j * 8 + 2 * q;
-        bv[j][0] = col < s.N ? __ldg(brow + col) : 0.0;
-        bv[j][1] = col + 1 < s.N ? __ldg(brow + col + 1) : 0.0;
+        const double2 b2 = *reinterpret_cast<const double2*>(bsl + qq * BN + wn * WN + j * 8 + 2 * q);
+        bv[j][0] = b2.x;
+        bv[j][1] = b2.y;
       }
 #pragma unroll
       for (int i = 0; i < MI; ++i) {

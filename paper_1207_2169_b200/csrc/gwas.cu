@@ -319,7 +319,7 @@ template <typename TA, int BN, int STAGES, bool SQ, bool FUSE = false>
 gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw::GemmShape& s, cudaStream_t st) {
   static bool attr_set = false;  // per instantiation (the library binds one device per process)
   constexpr size_t smem = gemm_smem_bytes<TA, BN, STAGES>();
-  static_assert(!FUSE || (size_t)(BN / 32) * kBM * gw::FUSE_MAX_NQ * 8 <=
+  static_assert(!FUSE || (size_t)((BN / 32) * kBM + BN) * gw::FUSE_MAX_NQ * 8 <=
                              (size_t)STAGES * (gw::GemmSmem<TA, kBM, BN>::kAStride + gw::GemmSmem<TA, kBM, BN>::kBStride),
                 "fused-K2 reduction buffer must fit in the stage buffers");
   auto kern = gw::gemm_tn_dmma<TA, kBM, BN, STAGES, SQ, FUSE>;

@@ -435,13 +435,13 @@ def test_host_outputs_stream_back(c0, i8, ovl, mode):
 
 
 # ------------------------------------------------------------------ NEXT-2: K2 fused into K1's epilogue
-@pytest.mark.parametrize("i8,alg,n,p,t,k", [(0, "eig", 200, 4, 4, 2000), (0, "eig", 333, 6, 4, 256),
+@pytest.mark.parametrize("i8,alg,n,p,t,k", [(0, "eig", 200, 4, 4, 2000), (0, "eig", 333, 5, 4, 256), (0, "eig", 300, 6, 4, 256),
                                             (8, "eig", 200, 4, 4, 512), (8, "eig", 517, 3, 8, 300),
                                             (0, "chol", 333, 4, 1, 256), (8, "chol", 200, 5, 1, 700),
                                             (0, "eig", 1000, 4, 1, 8192)])
 def test_fused_k2_matches_oracle_and_unfused(i8, alg, n, p, t, k):
     """Few traits: K2 contracted in K1's epilogue (fuse_k2, default) vs the separate K2 product and the oracle.
-    t (p + 2) = 32 at (333, 6, 4) is the FP64 fusion limit; (517, 3, 8) the int8 one."""
+    t (p + 2) = 28 at (333, 5, 4) is the FP64 fusion limit (32 at (300, 6, 4): unfused); (517, 3, 8) the int8 one."""
     cfg = datagen.custom_config(n=n, p=p, m=900, t=t, index=400 + n + t)
     ds = datagen.dataset(cfg)
     XR = datagen.xr_dosages(cfg, ld=_ld(n))
