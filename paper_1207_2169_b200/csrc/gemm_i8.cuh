@@ -53,6 +53,7 @@ struct I8Shape {
   // K2b fused into the epilogue (ft <= I8_FUSE_T traits; ft = 0: off): the C_a tiles are not
   // stored; each thread accumulates P[tn][row][j] = sum_{c in tile} X_R'[c, row]^2 d_j[c] (d_j = row j of fD, ld fld)
   // for its row, and fused_k2_reduce sums the partials over the C_a tiles in fixed order.
+  int square_a;       // store X_R'^2 in C_a (unfused int8 mode: K2b = (X_R'^2)^T D needs no squaring in its loop)
   int ft;
   const double* fD;
   long long fld;
@@ -178,7 +179,11 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
 #pragma unroll
       for (int c = 0; c < 16; c += 2) {
         const int e0 = __ldg(s.exps + oc0 + j0 + c), e1 = __ldg(s.exps + oc0 + j0 + c + 1);
-        const double x0 = scalbn(acc[c], e0 - 7), x1 = scalbn(acc[c + 1], e1 - 7);
+        double x0 = scalbn(acc[c], e0 - 7), x1 = scalbn(acc[c + 1], e1 - 7);
+        if (in_a && s.square_a) {  // the int8 mode needs X_R' only squared (K2b): store X_R'^2, K2b is then plain
+          x0 *= x0;
+          x1 *= x1;
+        }
         const int col = cbase + c;
         if (col + 1 < cmax) {
           *reinterpret_cast<double2*>(crow + col) = make_double2(x0, x1);

@@ -501,6 +501,7 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   s.group_m = 64;
   s.tri_tiles = (int)tri_tiles;
   if (ft < 0 || ft > gw::I8_FUSE_T) return fail(GWAS_E_ARG, "bad fused-K2b trait count");
+  s.square_a = ft == 0 ? 1 : 0;
   s.ft = ft;
   s.fD = fD;
   s.fld = fld;
@@ -1123,8 +1124,9 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
             fpart, fstride, (int)(d.na_pad / gw::I8_NB), (int)cols, (int)d.t, 0, (int)d.nsq, c2, d.ldc2);
         CKC(cudaGetLastError());
       } else {
-        CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, 0, cs2,
-                    16, splitbuf));
+        // xrp holds X_R'^2 (squared in K1i's epilogue), so this is a plain product (nsq = N: no squaring)
+        CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, d.t,
+                    cs2, 16, splitbuf));
       }
       CKG(c->toc(cs2));
     }
