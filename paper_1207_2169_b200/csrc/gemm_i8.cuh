@@ -129,13 +129,40 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+constexpr int EPI_CW = 8;  // output columns per TMEM drain chunk (S x 8 int32 registers in flight)
+
 // Epilogue (warps 4-7): warp w drains TMEM lanes 32 (w % 4) .. +31 (= tile rows), recombines the S digit
 // accumulators of each output column (Horner in 2^-7, fp64), scales by 2^(e-7) and stores fp64.
+// Per-tile operands of the epilogue, staged in shared memory by the epilogue warps while the MMAs run (each was
+// otherwise an L2 round trip inside the drain loop, exposed once per column chunk).
+struct I8EpiSmem {
+  int exps[I8_NB];
+  double d[I8_FUSE_T][I8_NB];
+};
+constexpr int I8_EPI_SMEM = (int)sizeof(I8EpiSmem);
+
 __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base, uint64_t* tmem_full, int m0, int tn,
-                                            int warp, int lane) {
+                                            int warp, int lane, I8EpiSmem* es) {
   // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = tile rows
   const int q = warp & 3;
   const int row = m0 + q * 32 + lane;
+  {
+    const int et = threadIdx.x - 128;  // 0..127 over the four epilogue warps
+    const int oc = tn * I8_NB;
+    if (et < I8_NB) es->exps[et] = __ldg(s.exps + oc + et);
+    if (tn < s.na_tiles && s.ft > 0)
+      for (int idx = et; idx < s.ft * I8_NB; idx += 128) {
+        const int jj = idx / I8_NB, c = idx - jj * I8_NB;
+        es->d[jj][c] = oc + c < s.na ? __ldg(s.fD + jj * s.fld + oc + c) : 0.0;
+      }
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the four epilogue warps only
+  }
   mbar_wait(tmem_full, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
@@ -146,30 +173,31 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
 #pragma unroll
   for (int jj = 0; jj < I8_FUSE_T; ++jj) part[jj] = 0.0;
 #pragma unroll 1
-  for (int j0 = 0; j0 < I8_NB; j0 += 16) {
-    double acc[16];
-    int32_t v[16];
-    tmem_ld16(tl + (I8_SLICES - 1) * I8_NB + j0, v);
+  for (int j0 = 0; j0 < I8_NB; j0 += EPI_CW) {
+    // all S digit planes of EPI_CW columns in flight at once, one wait (the drain is otherwise a chain of S
+    // dependent TMEM round trips per chunk, exposed because the accumulators fill TMEM and nothing overlaps them)
+    int32_t v[I8_SLICES][EPI_CW];
+#pragma unroll
+    for (int sl = 0; sl < I8_SLICES; ++sl) tmem_ld8(tl + sl * I8_NB + j0, v[sl]);
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    double acc[EPI_CW];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) acc[c] = (double)v[c];
+    for (int c = 0; c < EPI_CW; ++c) {
+      double a = (double)v[I8_SLICES - 1][c];
 #pragma unroll
-    for (int sl = I8_SLICES - 2; sl >= 0; --sl) {
-      tmem_ld16(tl + sl * I8_NB + j0, v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < 16; ++c) acc[c] = fma(acc[c], 0.0078125, (double)v[c]);  // acc * 2^-7 + I_s
+      for (int sl = I8_SLICES - 2; sl >= 0; --sl) a = fma(a, 0.0078125, (double)v[sl][c]);  // a * 2^-7 + I_s
+      acc[c] = a;
     }
     if (fuse) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < EPI_CW; ++c) {
         const int col = oc0 + j0 + c;
         if (col < s.na) {
-          const double x = scalbn(acc[c], __ldg(s.exps + col) - 7);
+          const double x = scalbn(acc[c], es->exps[j0 + c] - 7);
           const double x2 = x * x;
 #pragma unroll
           for (int jj = 0; jj < I8_FUSE_T; ++jj)
-            if (jj < s.ft) part[jj] = fma(x2, __ldg(s.fD + jj * s.fld + col), part[jj]);
+            if (jj < s.ft) part[jj] = fma(x2, es->d[jj][j0 + c], part[jj]);
         }
       }
     } else if (row < s.M) {
@@ -177,8 +205,8 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
       const int cbase = in_a ? oc0 + j0 : (tn - s.na_tiles) * I8_NB + j0;
       const int cmax = in_a ? s.na : s.nb;
 #pragma unroll
-      for (int c = 0; c < 16; c += 2) {
-        const int e0 = __ldg(s.exps + oc0 + j0 + c), e1 = __ldg(s.exps + oc0 + j0 + c + 1);
+      for (int c = 0; c < EPI_CW; c += 2) {
+        const int e0 = es->exps[j0 + c], e1 = es->exps[j0 + c + 1];
         double x0 = scalbn(acc[c], e0 - 7), x1 = scalbn(acc[c + 1], e1 - 7);
         if (in_a && s.square_a) {  // the int8 mode needs X_R' only squared (K2b): store X_R'^2, K2b is then plain
           x0 *= x0;
@@ -218,6 +246,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   uint64_t* empty = full + I8_STAGES;
   uint64_t* tmem_full = empty + I8_STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  I8EpiSmem* esm = reinterpret_cast<I8EpiSmem*>(tmem_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tm, tn;
@@ -303,7 +332,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       umma_commit(tmem_full);     // accumulators complete
     }
   } else if (warp >= 4) {
-    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane);
+    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -366,6 +395,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   uint64_t* empty = full + I8_STAGES2;
   uint64_t* tmem_full = empty + I8_STAGES2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  I8EpiSmem* esm = reinterpret_cast<I8EpiSmem*>(tmem_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -444,7 +474,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       umma_commit_2sm(tmem_full);
     }
   } else if (warp >= 4) {
-    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane);
+    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();

@@ -507,8 +507,8 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   s.fld = fld;
   s.fP = fP;
   s.fP_stride = fP_stride;
-  constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256;
-  constexpr size_t smem2 = 1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256;
+  constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256 + gw::I8_EPI_SMEM;
+  constexpr size_t smem2 = 1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256 + gw::I8_EPI_SMEM;
   static bool attr_set = false;
   if (!attr_set) {
     CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));

@@ -12,8 +12,12 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--cols", type=int, default=8192)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--int8-slices", type=int, default=0)
+ap.add_argument("--n", type=int, default=None, help="override n (config-0 generators at that size)")
+ap.add_argument("--t", type=int, default=None)
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.config]
+if a.n or a.t:
+    cfg = datagen.custom_config(n=a.n or cfg.n, p=cfg.p, m=max(a.cols, 1), t=a.t or cfg.t, S=2 * (a.n or cfg.n), index=500)
 ld = (cfg.n + 15) // 16 * 16
 ds = datagen.dataset(cfg, device="cuda")
 XR = torch.from_numpy(datagen.xr_dosages(cfg, 0, a.cols, ld=ld)).cuda()
@@ -23,4 +27,5 @@ out = eng.alloc_outputs(a.cols)
 for _ in range(a.reps):
     eng.run(XR, out=out)
 torch.cuda.synchronize()
-print(eng.kernel_times())
+kt = eng.kernel_times()
+print(f"n={cfg.n} t={cfg.t} cols={a.cols}", {k: round(v['ms'] / max(1, v['launches']), 4) for k, v in kt.items()})
