@@ -53,6 +53,8 @@ struct I8Shape {
   // K2b fused into the epilogue (ft <= I8_FUSE_T traits; ft = 0: off): the C_a tiles are not
   // stored; each thread accumulates P[tn][row][j] = sum_{c in tile} X_R'[c, row]^2 d_j[c] (d_j = row j of fD, ld fld)
   // for its row, and fused_k2_reduce sums the partials over the C_a tiles in fixed order.
+  int dbg;            // debug (GWAS_I8_DBG): 1 = skip TMEM loads in the epilogue, 2 = skip its stores
+  unsigned long long* trace;  // debug (GWAS_I8_TRACE): per-CTA %globaltimer stamps of the kernel phases, or null
   int square_a;       // store X_R'^2 in C_a (unfused int8 mode: K2b = (X_R'^2)^T D needs no squaring in its loop)
   int ft;
   const double* fD;
@@ -135,6 +137,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
                : "r"(taddr));
 }
 
+__device__ __forceinline__ void i8_stamp(const I8Shape& s, int slot) {
+  if (s.trace && blockIdx.x < 4096) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s.trace[blockIdx.x * 8 + slot] = globaltimer_ns();
+    s.trace[blockIdx.x * 8 + 7] = smid;
+  }
+}
+
 constexpr int EPI_CW = 8;  // output columns per TMEM drain chunk (S x 8 int32 registers in flight)
 
 // Epilogue (warps 4-7): warp w drains TMEM lanes 32 (w % 4) .. +31 (= tile rows), recombines the S digit
@@ -142,8 +153,8 @@ constexpr int EPI_CW = 8;  // output columns per TMEM drain chunk (S x 8 int32 r
 // Per-tile operands of the epilogue, staged in shared memory by the epilogue warps while the MMAs run (each was
 // otherwise an L2 round trip inside the drain loop, exposed once per column chunk).
 struct I8EpiSmem {
-  int exps[I8_NB];
-  double d[I8_FUSE_T][I8_NB];
+  double scale[I8_NB];  // 2^(e_c - 28) per output column of the tile
+  double d[I8_NB][I8_FUSE_T];  // fused D rows, column-major by trait (zero for traits >= ft)
 };
 constexpr int I8_EPI_SMEM = (int)sizeof(I8EpiSmem);
 
@@ -155,15 +166,16 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
   {
     const int et = threadIdx.x - 128;  // 0..127 over the four epilogue warps
     const int oc = tn * I8_NB;
-    if (et < I8_NB) es->exps[et] = __ldg(s.exps + oc + et);
+    if (et < I8_NB) es->scale[et] = scalbn(1.0, __ldg(s.exps + oc + et) - 28);
     if (tn < s.na_tiles && s.ft > 0)
-      for (int idx = et; idx < s.ft * I8_NB; idx += 128) {
+      for (int idx = et; idx < I8_FUSE_T * I8_NB; idx += 128) {
         const int jj = idx / I8_NB, c = idx - jj * I8_NB;
-        es->d[jj][c] = oc + c < s.na ? __ldg(s.fD + jj * s.fld + oc + c) : 0.0;
+        es->d[c][jj] = (jj < s.ft && oc + c < s.na) ? __ldg(s.fD + jj * s.fld + oc + c) : 0.0;
       }
     asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the four epilogue warps only
   }
   mbar_wait(tmem_full, 0);
+  if (threadIdx.x == 128) i8_stamp(s, 4);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
   const int oc0 = tn * I8_NB;  // first output column of the concatenated digit matrix
@@ -177,37 +189,49 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
     // all S digit planes of EPI_CW columns in flight at once, one wait (the drain is otherwise a chain of S
     // dependent TMEM round trips per chunk, exposed because the accumulators fill TMEM and nothing overlaps them)
     int32_t v[I8_SLICES][EPI_CW];
+    if (s.dbg != 1) {
 #pragma unroll
-    for (int sl = 0; sl < I8_SLICES; ++sl) tmem_ld8(tl + sl * I8_NB + j0, v[sl]);
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      for (int sl = 0; sl < I8_SLICES; ++sl) tmem_ld8(tl + sl * I8_NB + j0, v[sl]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    } else {
+#pragma unroll
+      for (int sl = 0; sl < I8_SLICES; ++sl)
+#pragma unroll
+        for (int c = 0; c < EPI_CW; ++c) v[sl][c] = lane + sl + c + j0;
+    }
+    // exact integer recombination of the digit accumulators in two 4-digit halves (|.| < 2^53 each, so both
+    // convert exactly), one fp64 rounding (the fma), then the exact power-of-two column scale 2^(e - 28):
+    //   x = sum_s I_s 2^(-7(s+1)) 2^e = (hi + lo 2^-28) 2^(e - 28),  hi = sum_{s<4} I_s 2^(7(3-s)),
+    //   lo = sum_{s>=4} I_s 2^(7(7-s))
+    static_assert(I8_SLICES == 8, "two 4-digit halves");
     double acc[EPI_CW];
 #pragma unroll
     for (int c = 0; c < EPI_CW; ++c) {
-      double a = (double)v[I8_SLICES - 1][c];
-#pragma unroll
-      for (int sl = I8_SLICES - 2; sl >= 0; --sl) a = fma(a, 0.0078125, (double)v[sl][c]);  // a * 2^-7 + I_s
-      acc[c] = a;
+      const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 + v[3][c];
+      const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 + v[7][c];
+      acc[c] = fma((double)lo, 0x1p-28, (double)hi) * es->scale[j0 + c];
     }
     if (fuse) {
 #pragma unroll
       for (int c = 0; c < EPI_CW; ++c) {
-        const int col = oc0 + j0 + c;
-        if (col < s.na) {
-          const double x = scalbn(acc[c], es->exps[j0 + c] - 7);
-          const double x2 = x * x;
+        // the trait loop runs over all I8_FUSE_T slots (zero rows beyond ft, zero columns beyond na): no predicates,
+        // and the column's 8 D values arrive as 4 independent 16-byte loads instead of a load->fma chain
+        const double x2 = acc[c] * acc[c];
+        const double2* dc = reinterpret_cast<const double2*>(es->d[j0 + c]);
 #pragma unroll
-          for (int jj = 0; jj < I8_FUSE_T; ++jj)
-            if (jj < s.ft) part[jj] = fma(x2, es->d[jj][j0 + c], part[jj]);
+        for (int jj = 0; jj < I8_FUSE_T; jj += 2) {
+          const double2 dd = dc[jj / 2];
+          part[jj] = fma(x2, dd.x, part[jj]);
+          part[jj + 1] = fma(x2, dd.y, part[jj + 1]);
         }
       }
-    } else if (row < s.M) {
+    } else if (row < s.M && s.dbg != 2) {
       double* crow = in_a ? s.Ca + (long long)row * s.lda_c : s.Cb + (long long)row * s.ldb_c;
       const int cbase = in_a ? oc0 + j0 : (tn - s.na_tiles) * I8_NB + j0;
       const int cmax = in_a ? s.na : s.nb;
 #pragma unroll
       for (int c = 0; c < EPI_CW; c += 2) {
-        const int e0 = es->exps[j0 + c], e1 = es->exps[j0 + c + 1];
-        double x0 = scalbn(acc[c], e0 - 7), x1 = scalbn(acc[c + 1], e1 - 7);
+        double x0 = acc[c], x1 = acc[c + 1];
         if (in_a && s.square_a) {  // the int8 mode needs X_R' only squared (K2b): store X_R'^2, K2b is then plain
           x0 *= x0;
           x1 *= x1;
@@ -249,6 +273,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   I8EpiSmem* esm = reinterpret_cast<I8EpiSmem*>(tmem_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) i8_stamp(s, 0);
   int tm, tn;
   const uint32_t crank = CL > 1 ? cluster_ctarank() : 0u;
   {
@@ -287,6 +312,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   if constexpr (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) i8_stamp(s, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -313,6 +339,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       for (int kb = 0; kb < KB; ++kb) {
         const int st = kb % I8_STAGES;
         mbar_wait(&full[st], (kb / I8_STAGES) & 1);
+        if (kb == 0) i8_stamp(s, 2);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t a0 = smem_u32(sA + st * A_BYTES);
         const uint32_t b0 = smem_u32(sB + st * B_BYTES);
@@ -330,13 +357,16 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         else umma_commit_mc(&empty[st], (uint16_t)((1u << CL) - 1));
       }
       umma_commit(tmem_full);     // accumulators complete
+      i8_stamp(s, 3);
     }
   } else if (warp >= 4) {
     i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
+    if (threadIdx.x == 128) i8_stamp(s, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
+  if (threadIdx.x == 0) i8_stamp(s, 6);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(512));

@@ -501,6 +501,14 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   s.group_m = 64;
   s.tri_tiles = (int)tri_tiles;
   if (ft < 0 || ft > gw::I8_FUSE_T) return fail(GWAS_E_ARG, "bad fused-K2b trait count");
+  // GWAS_I8_TRACE=<file>: debug phase stamps of the first 4096 CTAs of every launch, appended to <file>
+  static const char* trace_path = getenv("GWAS_I8_TRACE");
+  static unsigned long long* trace_dev = nullptr;
+  if (trace_path && !trace_dev) CKC(cudaMalloc(&trace_dev, sizeof(unsigned long long) * 4096 * 8));
+  s.trace = trace_path ? trace_dev : nullptr;
+  if (trace_dev) CKC(cudaMemsetAsync(trace_dev, 0, sizeof(unsigned long long) * 4096 * 8, st));
+  static const int dbg_env = getenv("GWAS_I8_DBG") ? atoi(getenv("GWAS_I8_DBG")) : 0;
+  s.dbg = dbg_env;
   s.square_a = ft == 0 ? 1 : 0;
   s.ft = ft;
   s.fD = fD;
@@ -538,6 +546,15 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
     else CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4>, ma, mb, s));
   }
   CKC(cudaGetLastError());
+  if (trace_dev) {
+    std::vector<unsigned long long> h(4096 * 8);
+    CKC(cudaStreamSynchronize(st));
+    CKC(cudaMemcpy(h.data(), trace_dev, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(trace_path, "ab")) {
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      fclose(f);
+    }
+  }
   return GWAS_OK;
 }
 

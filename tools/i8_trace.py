@@ -1,0 +1,23 @@
+"""Summarise GWAS_I8_TRACE phase stamps of the int8 kernel (debug).  Usage: python tools/i8_trace.py trace.bin
+Slots per CTA: 0 entry, 1 after TMEM alloc + barrier init, 2 first stage landed (MMA thread), 3 last commit issued,
+4 epilogue sees accumulators, 5 epilogue done, 6 before dealloc, 7 smid."""
+import sys
+import numpy as np
+a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 4096, 8)
+for li, L in enumerate(a):
+    v = L[L[:, 0] > 0].astype(np.int64)
+    if not len(v):
+        continue
+    t0 = v[:, 0].min()
+    d = lambda i, j: np.median(v[:, j] - v[:, i]) / 1e3
+    print(f"launch {li}: {len(v)} CTAs, span {(v[:, 6].max() - t0) / 1e3:.1f} us; median us: setup {d(0, 1):.2f} "
+          f"first-data {d(1, 2):.2f} mainloop {d(2, 3):.2f} commit->epi {d(3, 4):.2f} epilogue {d(4, 5):.2f} "
+          f"tail {d(5, 6):.2f} total {d(0, 6):.2f}")
+    # gaps between consecutive CTAs on the same SM
+    gaps = []
+    for sm in np.unique(v[:, 7]):
+        w = v[v[:, 7] == sm]
+        w = w[np.argsort(w[:, 0])]
+        gaps += list((w[1:, 0] - w[:-1, 6]) / 1e3)
+    if gaps:
+        print(f"   launch gap between CTAs on one SM: median {np.median(gaps):.2f} us, p90 {np.percentile(gaps, 90):.2f}")
