@@ -94,6 +94,13 @@ typedef struct {
                               contracted inside K1's epilogue per column tile, so X_R' never
                               goes to HBM; a fixed-order reduction finishes it.  0: separate K2 product.  A run-time
                               choice (not part of the state); results differ from the unfused path only by rounding. */
+  int32_t trait_rank;      /* 0 (default): the exact per-trait weights D_j of Alg. 4 line 6 in K2 (the paper's design).
+                              -1: low-rank trait weights (reading L1, CLAK-Eig only, t >= 16): setup
+                              factors D = [d_1 .. d_t] = U S V^T (cuSOLVER gesvd), keeps the r <= 64 singular
+                              triplets above 1e-15 s_0 (r rounded up to 8) and K2 contracts X_R' against the p r + t + r
+                              columns [U_r (.) X_L'_f | d_j (.) y'_j | U_r] instead of t (p + 2); a K = r product with
+                              W = S_r V_r^T restores the per-trait terms.  Error vs the exact weights ~ 1e-13 relative.
+                              Kept exact when it would not shrink the products (2 r >= t).  Part of the state. */
 } gwas_options;
 
 /* Fills the defaults listed above (device 0, u8 X_R). */
@@ -140,6 +147,10 @@ GWAS_API gwas_status gwas_setup_estimate(const gwas_options* opt, int64_t n, int
                                 double* h2_out, double* sigma2_out, double* loglik_out,
                                 void* state_dev, size_t state_bytes, void* work_dev, size_t work_bytes,
                                 gwas_ctx** out);
+
+/* Low-rank trait weights chosen at setup: *r = kept rank (0 = exact weights), *s0 / *s_r = largest singular value
+ * of D and the first dropped one (either may be NULL). */
+GWAS_API gwas_status gwas_trait_rank(gwas_ctx* ctx, int32_t* r, double* s0, double* s_r);
 
 /* Event time (ms) of the estimation kernels of gwas_setup_estimate (0 for a gwas_setup context). */
 GWAS_API gwas_status gwas_estimate_ms(gwas_ctx* ctx, double* ms);

@@ -19,7 +19,7 @@ ALG_EIG, ALG_CHOL = 0, 1
 EST_ML, EST_REML = 0, 1
 NUM_TIMERS = 4
 
-EXPORTS = ["gwas_default_options", "gwas_state_bytes", "gwas_workspace_bytes", "gwas_setup", "gwas_setup_estimate", "gwas_estimate_ms", "gwas_attach",
+EXPORTS = ["gwas_default_options", "gwas_state_bytes", "gwas_workspace_bytes", "gwas_setup", "gwas_setup_estimate", "gwas_estimate_ms", "gwas_trait_rank", "gwas_attach",
            "gwas_run", "gwas_timings", "gwas_kernel_times", "gwas_gemm_tn", "gwas_destroy", "gwas_last_error",
            "gwas_version"]
 
@@ -29,7 +29,8 @@ class GwasOptions(C.Structure):
                 ("var_convention", C.c_int32), ("block_cols", C.c_int64), ("eps_spd", C.c_double),
                 ("eps_collinear", C.c_double), ("compute_stream", C.c_void_p), ("copy_stream", C.c_void_p),
                 ("timing", C.c_int32), ("int8_slices", C.c_int32),
-                ("overlap", C.c_int32), ("algorithm", C.c_int32), ("fuse_k2", C.c_int32)]
+                ("overlap", C.c_int32), ("algorithm", C.c_int32), ("fuse_k2", C.c_int32),
+                ("trait_rank", C.c_int32)]
 
 
 class GwasError(RuntimeError):
@@ -52,6 +53,7 @@ def _load():
         "gwas_setup": (C.c_int, [opt, i64, i64, i64, P, P, P, P, P, P, sz, P, sz, C.POINTER(P)]),
         "gwas_setup_estimate": (C.c_int, [opt, i64, i64, i64, P, P, P, i32, P, P, P, P, sz, P, sz, C.POINTER(P)]),
         "gwas_estimate_ms": (C.c_int, [P, dp]),
+        "gwas_trait_rank": (C.c_int, [P, C.POINTER(C.c_int32), dp, dp]),
         "gwas_attach": (C.c_int, [opt, i64, i64, i64, P, sz, P, sz, C.POINTER(P)]),
         "gwas_run": (C.c_int, [P, i64, P, i64, P, P, P]),
         "gwas_timings": (C.c_int, [P, dp, dp, dp]),

@@ -47,7 +47,8 @@ class Gwas:
     def __init__(self, n: int, p: int, t: int, *, device: int = 0, xr_dtype: str = "u8", output_mode: str = "snp",
                  var_convention: str = "textbook", block_cols: int = 8192, timing: bool = False,
                  eps_spd: float = 1e-10, eps_collinear: float = 1e-10, compute_stream=None, copy_stream=None,
-                 int8_slices: int = 0, overlap: bool = False, algorithm: str = "eig", fuse_k2: bool = True):
+                 int8_slices: int = 0, overlap: bool = False, algorithm: str = "eig", fuse_k2: bool = True,
+                 trait_rank: int = 0):
         self.n, self.p, self.t = int(n), int(p), int(t)
         self.w = self.p + 1
         self.device = torch.device("cuda", device)
@@ -70,6 +71,7 @@ class Gwas:
         o.overlap = 1 if overlap else 0
         o.algorithm = _ALG[algorithm]
         o.fuse_k2 = 1 if fuse_k2 else 0
+        o.trait_rank = int(trait_rank)
         self.opt = o
         self.state_bytes = lib.gwas_state_bytes(self.n, self.p, self.t, C.byref(o))
         if self.state_bytes == 0:
@@ -119,6 +121,12 @@ class Gwas:
                                           self.state.data_ptr(), self.state_bytes, self.work.data_ptr(),
                                           self.work_bytes, C.byref(self._ctx)))
         return {"h2": h2, "sigma2": s2, "loglik": ll}
+
+    def trait_rank(self):
+        """(r, s0, s_r): the low-rank trait-weight rank chosen at setup (0 = exact weights) and the singular values."""
+        r, s0, sr = C.c_int32(), C.c_double(), C.c_double()
+        check(lib.gwas_trait_rank(self._ctx, C.byref(r), C.byref(s0), C.byref(sr)))
+        return r.value, s0.value, sr.value
 
     def estimate_ms(self) -> float:
         ms = C.c_double()

@@ -27,6 +27,8 @@ namespace {
 constexpr uint64_t kMagic = 0x4b414c4353415747ull;  // "GWASCLAK"
 constexpr int64_t kVersion = 1;
 constexpr int kPMax = 12;
+constexpr int kLrMax = 64;          // largest trait-weight rank kept (low-rank mode)
+constexpr double kLrTol = 1e-15;    // singular values of D below kLrTol * s_0 are dropped (reading L1)
 
 thread_local std::string g_err;
 
@@ -71,6 +73,11 @@ struct StateHeader {
   int64_t off_Z, off_W, off_B2, off_Lpk, off_v, off_s2, off_betaT, off_dinv, total;
   int32_t int8_slices, algorithm;
   int64_t na_pad, nlin, nlin_pad, off_dig, off_exps;  // int8-sliced mode: digit matrix of [Z | Z B_op] + 2^e
+  // low-rank trait weights (opt.trait_rank): D ~ U_r W with r = lr_r (0: exact D); B2 then holds
+  // [U_r (.) X_L'_f (p r rows) | d_j (.) y'_j (t rows) | pad to lr_nsq | U_r (r rows)], W^T at off_wt (t x r)
+  int32_t trait_rank, lr_r;
+  int64_t lr_nsq, lr_nlin, off_wt;
+  double lr_s0, lr_sr;  // largest kept / first dropped singular value of D (diagnostics)
 };
 constexpr size_t kHeaderBytes = 512;
 static_assert(sizeof(StateHeader) <= kHeaderBytes, "header");
@@ -81,6 +88,8 @@ struct Dims {
   int64_t per_pair;                // outputs per pair: 1 (SNP mode) or p + 1 (full mode)
   int i8;                          // int8-sliced mode
   int64_t na_pad, nlin, nlin_pad;  // digit-matrix column blocks (multiples of 64)
+  bool lr;                         // low-rank trait weights requested (state reserves room; setup decides r)
+  int64_t ldg2;                    // low-rank K2 output row stride (p rmax + t + 32 + rmax)
   bool fuse;                       // K2 fused into K1's epilogue (few traits, opt.fuse_k2)
   int64_t fnq, ftiles;             // fused K2 columns per pair-row; max K1 column tiles (partials per block)
 };
@@ -104,6 +113,8 @@ Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   d.nlin_pad = round_up(d.nlin, gw::I8_NB);
   // NEXT-2 fusion: FP64 mode contracts all t (p + 2) K2 columns in K1's epilogue, the int8 mode only the t squared
   // columns (its linear K2 terms already come out of K1i)
+  d.lr = o->trait_rank != 0 && o->algorithm == GWAS_ALG_EIG;
+  d.ldg2 = round_up(p * kLrMax + t + 32 + kLrMax, 2);
   d.fnq = d.i8 ? t : t * (p + 2);
   d.fuse = o->fuse_k2 != 0 && (d.i8 ? t <= gw::I8_FUSE_T : d.fnq <= gw::FUSE_MAX_NQ);
   d.ftiles = d.i8 ? d.na_pad / gw::I8_NB : (n + 63) / 64;
@@ -148,12 +159,14 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
     h.off_dig = take((size_t)((d.na_pad + d.nlin_pad) / gw::I8_NB) * gw::I8_BROWS * d.kpad);
     h.off_exps = take(sizeof(int) * (d.na_pad + d.nlin_pad));
   }
+  h.trait_rank = o->trait_rank;
+  if (d.lr) h.off_wt = take(sizeof(double) * d.t * kLrMax);
   h.total = (int64_t)off;
   return h;
 }
 
 struct RunLayout {
-  size_t stage[2], xrp[2], c2[2], split[2], outb[2], fp[2], total;
+  size_t stage[2], xrp[2], c2[2], split[2], outb[2], fp[2], g2[2], total;
   size_t out_bytes;  // per staging set: b, var (8 * per_pair each) + status (1) per pair of a block
 };
 // overlap mode double-buffers the rotated block and the K2 output so block b+1's K1 can run beside block b's K2/K3
@@ -177,6 +190,11 @@ RunLayout run_layout(const Dims& d, bool overlap) {
   r.out_bytes = (size_t)d.kb * d.t * (16 * d.per_pair + 1);
   r.outb[0] = take(r.out_bytes);
   r.outb[1] = take(r.out_bytes);
+  r.g2[0] = r.g2[1] = 0;
+  if (d.lr) {  // low-rank K2 output [U_r-projected fields | y | pad | squared]
+    r.g2[0] = take(sizeof(double) * d.ldg2 * d.kb);
+    r.g2[1] = overlap ? take(sizeof(double) * d.ldg2 * d.kb) : r.g2[0];
+  }
   r.fp[0] = r.fp[1] = 0;
   if (d.fuse) {  // per-tile partial sums of the fused K2
     r.fp[0] = take(sizeof(double) * d.ftiles * d.kb * d.fnq);
@@ -188,8 +206,9 @@ RunLayout run_layout(const Dims& d, bool overlap) {
 
 struct SetupLayout {
   size_t xlpad, ypad, xlp, yp, stl, h2, s2, err, info, est_rec, est_ll, est_gs, work, zt, blin, total;
+  size_t lr_a, lr_u, lr_vt, lr_s, lr_work, lr_b2;  // low-rank: SVD of D and the rebuilt operand
 };
-SetupLayout setup_layout(const Dims& d, int64_t lwork) {
+SetupLayout setup_layout(const Dims& d, int64_t lwork, int64_t lr_lwork = 0) {
   SetupLayout s;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -215,6 +234,15 @@ SetupLayout setup_layout(const Dims& d, int64_t lwork) {
     s.zt = take(sizeof(double) * d.kpad * d.kpad);
     s.blin = take(sizeof(double) * d.nlin * d.kpad);
   }
+  s.lr_a = s.lr_u = s.lr_vt = s.lr_s = s.lr_work = s.lr_b2 = 0;
+  if (d.lr) {
+    s.lr_a = take(sizeof(double) * d.kpad * d.t);
+    s.lr_u = take(sizeof(double) * d.kpad * d.t);
+    s.lr_vt = take(sizeof(double) * d.t * d.t);
+    s.lr_s = take(sizeof(double) * d.t);
+    s.lr_work = take(sizeof(double) * std::max<int64_t>(lr_lwork, 1));
+    s.lr_b2 = take(sizeof(double) * d.n2 * d.kpad);
+  }
   s.total = off;
   return s;
 }
@@ -234,6 +262,7 @@ gwas_status check_sizes(int64_t n, int64_t p, int64_t t, const gwas_options* o) 
   const int64_t t_p2 = t * (p + 2) + 8;
   if (t_p2 > (1ll << 31) - 1) return fail(GWAS_E_ARG, "t too large");
   if (o->algorithm != GWAS_ALG_EIG && o->algorithm != GWAS_ALG_CHOL) return fail(GWAS_E_ARG, "bad algorithm");
+  if (o->trait_rank != 0 && o->trait_rank != -1) return fail(GWAS_E_ARG, "trait_rank must be 0 (exact) or -1 (auto)");
   if (o->algorithm == GWAS_ALG_CHOL && t != 1)
     return fail(GWAS_E_ARG, "CLAK-Chol (Alg. 3) is the single-trait algorithm: t = %lld != 1", (long long)t);
   if (o->int8_slices != 0) {
@@ -270,6 +299,21 @@ gwas_status solver_lwork(const gwas_options* o, int64_t n, int64_t kpad, int64_t
   }
   cusolverDnDestroy(h);
   if (s != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "cuSOLVER bufferSize status %d", (int)s);
+  return GWAS_OK;
+}
+
+// Device workspace (doubles) of cusolverDnDgesvd on the n x t trait-weight matrix D (low-rank mode), 0 if unused.
+gwas_status lr_lwork(const gwas_options* o, const Dims& d, int64_t* lwork) {
+  *lwork = 0;
+  if (!d.lr || d.t > d.n) return GWAS_OK;
+  CKC(cudaSetDevice(o->device));
+  cusolverDnHandle_t h;
+  CKS(cusolverDnCreate(&h));
+  int lw = 0;
+  cusolverStatus_t st = cusolverDnDgesvd_bufferSize(h, (int)d.n, (int)d.t, &lw);
+  cusolverDnDestroy(h);
+  if (st != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "cusolverDnDgesvd_bufferSize status %d", (int)st);
+  *lwork = lw;
   return GWAS_OK;
 }
 
@@ -700,6 +744,24 @@ gwas_status ctx_init(gwas_ctx* c, const gwas_options* o, const Dims& d, const St
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+// Low-rank recombination (reading L1): c2[:, f t + j] = sum_r g2[:, f r + rr] W[rr, j] for the p X_L fields and
+// c2[:, nsq + j] = sum_r g2[:, lr_nsq + rr] W[rr, j] for the squared term (DMMA products with K = r).
+gwas_status lowrank_recombine(gwas_ctx* c, const double* g2, double* c2, int64_t cols, cudaStream_t st) {
+  const Dims& d = c->d;
+  const int64_t r = c->h.lr_r;
+  const double* wt = reinterpret_cast<const double*>(c->state + c->h.off_wt);
+  for (int64_t f = 0; f < d.p; ++f)
+    CKG(gemm_tn(false, g2 + f * r, d.ldg2, wt, r, c2 + f * d.t, d.ldc2, cols, d.t, r, d.t, st, 16));
+  CKG(gemm_tn(false, g2 + c->h.lr_nsq, d.ldg2, wt, r, c2 + d.nsq, d.ldc2, cols, d.t, r, d.t, st, 16));
+  return GWAS_OK;
+}
+}  // namespace
+
+extern "C" {
+
 void gwas_default_options(gwas_options* o) {
   if (!o) return;
   memset(o, 0, sizeof(*o));
@@ -731,7 +793,9 @@ size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options*
   int64_t lwork = 0;
   size_t host_ws = 0;
   if (solver_lwork(o, n, d.kpad, &lwork, &host_ws) != GWAS_OK) return 0;
-  return std::max(setup_layout(d, lwork).total, run_layout(d, o->overlap != 0).total);
+  int64_t lrw = 0;
+  if (lr_lwork(o, d, &lrw) != GWAS_OK) return 0;
+  return std::max(setup_layout(d, lwork, lrw).total, run_layout(d, o->overlap != 0).total);
 }
 
 }  // extern "C"
@@ -755,7 +819,9 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
   int64_t lwork = 0;
   size_t host_ws = 0;
   CKG(solver_lwork(o, n, d.kpad, &lwork, &host_ws));
-  SetupLayout sl = setup_layout(d, lwork);
+  int64_t lrw = 0;
+  CKG(lr_lwork(o, d, &lrw));
+  SetupLayout sl = setup_layout(d, lwork, lrw);
   RunLayout rl = run_layout(d, o->overlap != 0);
   if (state_bytes < (size_t)h.total) return fail(GWAS_E_NOMEM, "state %zu < %lld bytes", state_bytes, (long long)h.total);
   if (work_bytes < std::max(sl.total, rl.total))
@@ -901,6 +967,58 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
                                                                          o->eps_collinear, c->Lpk(), c->v(),
                                                                          c->betaT(), c->dinv(), derr + 1);
     CKC(cudaGetLastError());
+    // Low-rank trait weights (opt.trait_rank = -1, reading L1): D = U S V^T (gesvd), keep the r singular triplets
+    // above kLrTol s_0 (r rounded up to 8), and rebuild the K2 operand from U_r (p r + t + r rows instead of
+    // t (p + 2)); the run recombines with W = S_r V_r^T.  Skipped when it would not shrink the products.
+    c->h.lr_r = 0;
+    c->h.lr_nsq = d.nsq;
+    c->h.lr_nlin = d.nlin;
+    if (d.lr && t >= 16 && t <= n) {
+      double* A = reinterpret_cast<double*>(w + sl.lr_a);
+      double* U = reinterpret_cast<double*>(w + sl.lr_u);
+      double* VT = reinterpret_cast<double*>(w + sl.lr_vt);
+      double* S = reinterpret_cast<double*>(w + sl.lr_s);
+      CKC(cudaMemcpy2DAsync(A, sizeof(double) * d.kpad, c->B2() + d.nsq * d.kpad, sizeof(double) * d.kpad,
+                            sizeof(double) * n, t, cudaMemcpyDeviceToDevice, cs));
+      cusolverDnHandle_t hv;
+      CKS(cusolverDnCreate(&hv));
+      cusolverStatus_t sv = cusolverDnSetStream(hv, cs);
+      if (sv == CUSOLVER_STATUS_SUCCESS)
+        sv = cusolverDnDgesvd(hv, 'S', 'S', (int)n, (int)t, A, (int)d.kpad, S, U, (int)d.kpad, VT, (int)t,
+                              reinterpret_cast<double*>(w + sl.lr_work), (int)std::max<int64_t>(lrw, 1), nullptr,
+                              dinfo);
+      std::vector<double> hs(t);
+      CKC(cudaMemcpyAsync(hs.data(), S, sizeof(double) * t, cudaMemcpyDeviceToHost, cs));
+      int sinfo = 0;
+      CKC(cudaMemcpyAsync(&sinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, cs));
+      CKC(cudaStreamSynchronize(cs));
+      cusolverDnDestroy(hv);
+      if (sv != CUSOLVER_STATUS_SUCCESS || sinfo != 0)
+        return fail(GWAS_E_EIG, "gesvd of the trait weights: status %d info %d", (int)sv, sinfo);
+      int64_t r = 0;
+      while (r < t && hs[r] > kLrTol * hs[0]) ++r;
+      r = std::max<int64_t>(8, round_up(r, 8));
+      if (r <= kLrMax && 2 * r < t) {
+        const int64_t nsq_lr = round_up(p * r + t, 32);
+        double* nb2 = reinterpret_cast<double*>(w + sl.lr_b2);
+        dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)(nsq_lr + r));
+        gw::build_lowrank_b2<<<grid, 256, 0, cs>>>(U, d.kpad, xlp, c->B2(), (int)n, (int)p, (int)t, (int)d.kpad,
+                                                   (int)r, (int)nsq_lr, nb2);
+        CKC(cudaGetLastError());
+        CKC(cudaMemcpyAsync(c->B2(), nb2, sizeof(double) * (nsq_lr + r) * d.kpad, cudaMemcpyDeviceToDevice, cs));
+        gw::build_lowrank_wt<<<(unsigned)((t * r + 255) / 256), 256, 0, cs>>>(
+            S, VT, (int)t, (int)r, reinterpret_cast<double*>(c->state + c->h.off_wt));
+        CKC(cudaGetLastError());
+        c->h.lr_r = (int32_t)r;
+        c->h.lr_nsq = nsq_lr;
+        c->h.lr_nlin = p * r + t;
+        c->h.lr_s0 = hs[0];
+        c->h.lr_sr = r < t ? hs[r] : 0.0;
+      }
+      CKC(cudaMemcpyAsync(c->state, &c->h, sizeof(StateHeader), cudaMemcpyHostToDevice, cs));
+      CKC(cudaStreamSynchronize(cs));
+    }
+    const int64_t nlin_eff = c->h.lr_nlin, nlin_pad_eff = round_up(nlin_eff, gw::I8_NB);
     if (d.i8) {
       // sliced mode: B_lin = Z B_op (n x t(p+1), rows = output columns), then S-digit split of [Z | B_lin]
       double* zt = reinterpret_cast<double*>(w + sl.zt);
@@ -908,14 +1026,14 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
       gw::transpose_sq<<<dim3((unsigned)((d.kpad + 31) / 32), (unsigned)((d.kpad + 31) / 32)), dim3(32, 8), 0, cs>>>(
           c->Z(), zt, (int)d.kpad);
       CKC(cudaGetLastError());
-      CKG(gemm_tn(false, c->B2(), d.kpad, zt, d.kpad, blin, d.kpad, d.nlin, n, n, n, cs));
-      const size_t dig_bytes = (size_t)((d.na_pad + d.nlin_pad) / gw::I8_NB) * gw::I8_BROWS * d.kpad;
+      CKG(gemm_tn(false, c->B2(), d.kpad, zt, d.kpad, blin, d.kpad, nlin_eff, n, n, n, cs));
+      const size_t dig_bytes = (size_t)((d.na_pad + nlin_pad_eff) / gw::I8_NB) * gw::I8_BROWS * d.kpad;
       CKC(cudaMemsetAsync(c->dig(), 0, dig_bytes, cs));
-      CKC(cudaMemsetAsync(c->exps(), 0, sizeof(int) * (d.na_pad + d.nlin_pad), cs));
+      CKC(cudaMemsetAsync(c->exps(), 0, sizeof(int) * (d.na_pad + nlin_pad_eff), cs));
       gw::digitize_rows<<<(unsigned)n, 256, 0, cs>>>(c->Z(), d.kpad, (int)n, (int)n, 0, c->dig(), d.kpad, c->exps());
       CKC(cudaGetLastError());
-      gw::digitize_rows<<<(unsigned)d.nlin, 256, 0, cs>>>(blin, d.kpad, (int)d.nlin, (int)n, (int)d.na_pad, c->dig(),
-                                                           d.kpad, c->exps());
+      gw::digitize_rows<<<(unsigned)nlin_eff, 256, 0, cs>>>(blin, d.kpad, (int)nlin_eff, (int)n, (int)d.na_pad,
+                                                             c->dig(), d.kpad, c->exps());
       CKC(cudaGetLastError());
     }
     CKC(cudaEventRecord(e3, cs));
@@ -990,6 +1108,15 @@ gwas_status gwas_setup_estimate(const gwas_options* o, int64_t n, int64_t p, int
                     state_bytes, work_dev, work_bytes, out);
 }
 
+gwas_status gwas_trait_rank(gwas_ctx* c, int32_t* r, double* s0, double* s_r) {
+  g_err.clear();
+  if (!c || !r) return fail(GWAS_E_ARG, "NULL argument");
+  *r = c->h.lr_r;
+  if (s0) *s0 = c->h.lr_s0;
+  if (s_r) *s_r = c->h.lr_sr;
+  return GWAS_OK;
+}
+
 gwas_status gwas_estimate_ms(gwas_ctx* c, double* ms) {
   g_err.clear();
   if (!c || !ms) return fail(GWAS_E_ARG, "NULL argument");
@@ -1013,7 +1140,7 @@ gwas_status gwas_attach(const gwas_options* o, int64_t n, int64_t p, int64_t t, 
   CKC(cudaMemcpy(&got, state_dev, sizeof(got), cudaMemcpyDeviceToHost));
   if (got.magic != kMagic || got.version != kVersion || got.n != n || got.p != p || got.t != t ||
       got.total != want.total || got.output_mode != o->output_mode || got.var_convention != o->var_convention ||
-      got.int8_slices != o->int8_slices || got.algorithm != o->algorithm)
+      got.int8_slices != o->int8_slices || got.algorithm != o->algorithm || got.trait_rank != o->trait_rank)
     return fail(GWAS_E_STATE, "state header does not match (n, p, t, options)");
   gwas_ctx* c = new gwas_ctx();
   gwas_status st = ctx_init(c, o, d, got, state_dev, work_dev, work_bytes);
@@ -1045,6 +1172,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     return fail(GWAS_E_ARG, "host outputs must be page-locked (pinned)");
   const bool u8 = c->opt.xr_dtype == GWAS_XR_U8;
   const bool chol = c->opt.algorithm == GWAS_ALG_CHOL;
+  const int64_t lr_r = c->h.lr_r, lr_nsq = c->h.lr_nsq, lr_nlin = c->h.lr_nlin;
   const int64_t w = d.p + 1;
   const int64_t per_pair = c->opt.output_mode == GWAS_OUT_FULL ? w : 1;
   cudaStream_t cs = c->cs, ps = c->ps;
@@ -1062,6 +1190,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     double* xrp = reinterpret_cast<double*>(c->work + c->rl.xrp[set]);
     double* c2 = reinterpret_cast<double*>(c->work + c->rl.c2[set]);
     double* splitbuf = reinterpret_cast<double*>(c->work + c->rl.split[set]);
+    double* g2 = d.lr ? reinterpret_cast<double*>(c->work + c->rl.g2[set]) : nullptr;
     if (ovl) CKC(cudaStreamWaitEvent(cs, c->ev_set_free[set], 0));  // K2/K3 of block bi-2 done with this set
     const uint8_t* src = static_cast<const uint8_t*>(XR) + blk * ldx * (int64_t)d.es;
     const void* A = src;
@@ -1117,6 +1246,10 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
         gw::fused_k2_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, cs2>>>(
             fpart, fstride, k1_tiles, (int)cols, (int)d.fnq, (int)(d.t * (d.p + 1)), (int)d.nsq, c2, d.ldc2);
         CKC(cudaGetLastError());
+      } else if (lr_r > 0) {  // low-rank trait weights: the products against U_r, then the recombination with W
+        CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, g2, d.ldg2, cols, lr_nsq + lr_r, d.n, lr_nsq, cs2, 16,
+                    splitbuf));
+        CKG(lowrank_recombine(c, g2, c2, cols, cs2));
       } else {
         CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, 16, splitbuf));
       }
@@ -1124,8 +1257,9 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     } else {
       // K1i + K2a (int8-sliced, exact): X_R'^T = X_R^T Z and C[:, 0:t(p+1)] = X_R^T (Z B_op) in one launch
       CKG(c->tic(GWAS_K1, cs, &dummy));
-      CKG(launch_i8(A, lda, cols, d.n, c->dig(), d.kpad, (d.na_pad + d.nlin_pad) / gw::I8_NB, d.na_pad / gw::I8_NB,
-                    c->exps(), xrp, d.kpad, d.n, c2, d.ldc2, d.nlin, cs, chol ? d.na_pad / gw::I8_NB : 0,
+      CKG(launch_i8(A, lda, cols, d.n, c->dig(), d.kpad, (d.na_pad + round_up(lr_nlin, gw::I8_NB)) / gw::I8_NB,
+                    d.na_pad / gw::I8_NB, c->exps(), xrp, d.kpad, d.n, lr_r > 0 ? g2 : c2,
+                    lr_r > 0 ? d.ldg2 : d.ldc2, lr_nlin, cs, chol ? d.na_pad / gw::I8_NB : 0,
                     d.fuse ? (int)d.t : 0, c->B2() + d.nsq * d.kpad, d.kpad, fpart, fstride));
       CKG(c->toc(cs));
       if (s >= 0) CKC(cudaEventRecord(c->ev_free[s], cs));
@@ -1140,6 +1274,10 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
         gw::fused_k2_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, cs2>>>(
             fpart, fstride, (int)(d.na_pad / gw::I8_NB), (int)cols, (int)d.t, 0, (int)d.nsq, c2, d.ldc2);
         CKC(cudaGetLastError());
+      } else if (lr_r > 0) {  // low-rank: X_R'^2 against the r columns of U_r, then the recombination with W
+        CKG(gemm_tn(false, xrp, d.kpad, c->B2() + lr_nsq * d.kpad, d.kpad, g2 + lr_nsq, d.ldg2, cols, lr_r, d.n,
+                    lr_r, cs2, 16, splitbuf));
+        CKG(lowrank_recombine(c, g2, c2, cols, cs2));
       } else {
         // xrp holds X_R'^2 (squared in K1i's epilogue), so this is a plain product (nsq = N: no squaring)
         CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, d.t,
@@ -1151,6 +1289,8 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     gw::SchurArgs a;
     a.C = c2;
     a.ldc = d.ldc2;
+    a.Cy = lr_r > 0 ? g2 + d.p * lr_r : c2 + d.p * d.t;  // r_ij: the y field (kept apart in low-rank mode)
+    a.ldcy = lr_r > 0 ? d.ldg2 : d.ldc2;
     a.nsq = (int)d.nsq;
     a.cols = (int)cols;
     a.t = (int)d.t;

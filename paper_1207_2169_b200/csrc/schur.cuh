@@ -20,6 +20,8 @@ namespace gw {
 struct SchurArgs {
   const double* C;    // cols x ldc (row i = SNP i of the block)
   long long ldc;
+  const double* Cy;   // r_ij = Cy[i * ldcy + j] (= C + p t, ldc, unless the low-rank path keeps the y field apart)
+  long long ldcy;
   int nsq;            // column offset of the c_ij block
   int cols, t;
   const double* Lpk;  // [e][j], e = f(f+1)/2 + l (packed lower L_TL_j, row-major)
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(128) schur_solve(SchurArgs s) {
       uu += u[f] * u[f];
       uv += u[f] * v[f];
     }
-    const double r = __ldg(row + P * t + j);
+    const double r = __ldg(s.Cy + (long long)i * s.ldcy + j);
     const double c = __ldg(row + s.nsq + j);
     const double sigma = c - uu;
     int8_t st = 0;

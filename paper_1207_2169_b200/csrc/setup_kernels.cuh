@@ -114,3 +114,42 @@ __global__ void pad_columns(const double* __restrict__ src, long long ld_src, in
 }
 
 }  // namespace gw
+
+namespace gw {
+
+// Low-rank trait weights (reading L1): with D = U S V^T (cusolver gesvd, U n x t, ld ldu) truncated to r
+// columns, the K2 operand becomes (rows of kpad doubles, K-contiguous; entries k >= n are 0)
+//   row f r + rr (f < p) :  U[:, rr] * X_L'[:, f]          row p r + j :  B2_old row p t + j  (= d_j * y'_j)
+//   rows p r + t .. nsq_lr - 1 : 0                          row nsq_lr + rr :  U[:, rr]        (used with A∘A)
+// written to `out` (not in place: the y rows move up).
+__global__ void build_lowrank_b2(const double* __restrict__ U, long long ldu, const double* __restrict__ XLp,
+                                 const double* __restrict__ B2, int n, int p, int t, int kpad, int r, int nsq_lr,
+                                 double* __restrict__ out) {
+  const int row = blockIdx.y;
+  double* o = out + (long long)row * kpad;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (k < n) {
+      if (row < p * r) {
+        const int f = row / r, rr = row - f * r;
+        v = U[(long long)rr * ldu + k] * XLp[(long long)f * kpad + k];
+      } else if (row < p * r + t) {
+        v = B2[(long long)(p * t + (row - p * r)) * kpad + k];
+      } else if (row >= nsq_lr) {
+        v = U[(long long)(row - nsq_lr) * ldu + k];
+      }
+    }
+    o[k] = v;
+  }
+}
+
+// W^T (t x r, row j = the trait's r mixing weights): Wt[j][rr] = S[rr] VT[rr][j]  (VT column-major, ld t).
+__global__ void build_lowrank_wt(const double* __restrict__ S, const double* __restrict__ VT, int t, int r,
+                                 double* __restrict__ Wt) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= t * r) return;
+  const int j = idx / r, rr = idx - j * r;
+  Wt[idx] = S[rr] * VT[(long long)j * t + rr];
+}
+
+}  // namespace gw

@@ -12,8 +12,9 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("index,i8", [(1, 0), (2, 0), (3, 0), (4, 0), (1, 8), (2, 8), (3, 8), (4, 8)])
-def test_full_config_subsample(index, i8):
+@pytest.mark.parametrize("index,i8,lr", [(1, 0, 0), (2, 0, 0), (3, 0, 0), (4, 0, 0), (1, 8, 0), (2, 8, 0), (3, 8, 0),
+                                         (4, 8, 0), (2, 0, -1), (4, 0, -1), (2, 8, -1), (4, 8, -1)])
+def test_full_config_subsample(index, i8, lr):
     import paper_1207_2169_b200 as gw
     cfg = datagen.CONFIGS[index]
     dev = torch.device("cuda", 0)
@@ -22,8 +23,10 @@ def test_full_config_subsample(index, i8):
     xr = torch.empty((cfg.m, ld), dtype=torch.uint8, pin_memory=True)
     datagen.xr_dosages(cfg, ld=ld, out=xr.numpy())
     xr_dev = xr.to(dev)
-    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=8192, int8_slices=i8)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=8192, int8_slices=i8, trait_rank=lr)
     eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    rank = eng.trait_rank()[0]
+    assert (rank > 0) == (lr != 0)  # C2 / C4 (t = 1000) compress
     b, v, s = eng.run(xr_dev)
     snps, traits = datagen.subsample(cfg)
     idx_s = torch.from_numpy(snps).to(dev)
@@ -37,7 +40,7 @@ def test_full_config_subsample(index, i8):
     G = datagen.xr_columns(cfg, snps)
     ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
     eb, ev = compare(bs, vs, ss, ref)
-    print(f"C{index} int8_slices={i8}: {snps.size} SNPs x {traits.size} traits = {snps.size * traits.size} pairs, "
+    print(f"C{index} int8_slices={i8} trait_rank={rank}: {snps.size} SNPs x {traits.size} traits = {snps.size * traits.size} pairs, "
           f"max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
     assert snps.size * traits.size >= 10_000
     assert eb <= TOL_B and ev <= TOL_VAR

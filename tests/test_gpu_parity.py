@@ -457,3 +457,39 @@ def test_fused_k2_matches_oracle_and_unfused(i8, alg, n, p, t, k):
     other = _run(cfg, ds, dev, block_cols=128, int8_slices=i8, algorithm=alg)
     for x, y in zip(fused, other):
         np.testing.assert_array_equal(x, y)
+
+
+# ------------------------------------------------------------------ low-rank trait weights (reading L1)
+@pytest.mark.parametrize("i8,mode,ovl", [(0, "snp", False), (0, "full", True), (8, "snp", True), (8, "full", False)])
+def test_lowrank_trait_weights(i8, mode, ovl):
+    """trait_rank = -1: K2 against U_r of D = U S V^T (r << t) + the K = r recombination, vs the oracle's exact GLS."""
+    gw = _gw()
+    cfg = datagen.custom_config(n=240, p=4, m=700, t=96, index=451)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=256, int8_slices=i8, output_mode=mode, overlap=ovl,
+                  trait_rank=-1)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    r, s0, sr = eng.trait_rank()
+    assert 8 <= r <= 40 and sr <= 1e-15 * s0, (r, s0, sr)
+    b, v, s = eng.run(torch.from_numpy(XR).cuda())
+    torch.cuda.synchronize()
+    res = (b.cpu().numpy(), v.cpu().numpy(), s.cpu().numpy())
+    eng.close()
+    eb, ev = compare(*res, ref, full=mode == "full")
+    print(f"low-rank r={r} (i8={i8}, {mode}): max|db|/SE={eb:.2e} Var rel={ev:.2e}")
+    assert eb <= TOL_B and ev <= TOL_VAR
+    # a state copy attaches with the chosen rank; results identical
+    exact = _run(cfg, ds, torch.from_numpy(XR).cuda(), block_cols=256, int8_slices=i8, output_mode=mode)
+    np.testing.assert_array_equal(exact[2], res[2])
+
+
+def test_lowrank_skipped_for_few_traits():
+    gw = _gw()
+    cfg = datagen.custom_config(n=100, p=3, m=10, t=8, index=452)
+    ds = datagen.dataset(cfg)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, trait_rank=-1)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    assert eng.trait_rank()[0] == 0
+    eng.close()

@@ -14,6 +14,7 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--int8-slices", type=int, default=0)
 ap.add_argument("--n", type=int, default=None, help="override n (config-0 generators at that size)")
 ap.add_argument("--t", type=int, default=None)
+ap.add_argument("--trait-rank", type=int, default=0)
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.config]
 if a.n or a.t:
@@ -21,11 +22,13 @@ if a.n or a.t:
 ld = (cfg.n + 15) // 16 * 16
 ds = datagen.dataset(cfg, device="cuda")
 XR = torch.from_numpy(datagen.xr_dosages(cfg, 0, a.cols, ld=ld)).cuda()
-eng = gw.Gwas(cfg.n, cfg.p, cfg.t, block_cols=a.cols, timing=True, int8_slices=a.int8_slices)
+eng = gw.Gwas(cfg.n, cfg.p, cfg.t, block_cols=a.cols, timing=True, int8_slices=a.int8_slices,
+              trait_rank=a.trait_rank)
 eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
 out = eng.alloc_outputs(a.cols)
 for _ in range(a.reps):
     eng.run(XR, out=out)
 torch.cuda.synchronize()
 kt = eng.kernel_times()
+print("trait rank", eng.trait_rank(), eng.timings())
 print(f"n={cfg.n} t={cfg.t} cols={a.cols}", {k: round(v['ms'] / max(1, v['launches']), 4) for k, v in kt.items()})
