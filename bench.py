@@ -233,10 +233,10 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    def make_engine(i8, overlap, algorithm="eig"):
+    def make_engine(i8, overlap, algorithm="eig", trait_rank=0):
         """Rank 0 sets up (eig + precompute), the state is replicated by ONE broadcast, other ranks attach."""
         eng = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=overlap,
-                      algorithm=algorithm, fuse_k2=bool(args.fuse_k2))
+                      algorithm=algorithm, fuse_k2=bool(args.fuse_k2), trait_rank=trait_rank)
         info = {}
         if rank == 0:
             eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
@@ -254,7 +254,7 @@ def run_ours(args):
                 eng.attach()
         # a second, serial context on the same state (gwas_attach) times the kernels one by one
         ser = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, int8_slices=i8, overlap=False,
-                      algorithm=algorithm, fuse_k2=bool(args.fuse_k2))
+                      algorithm=algorithm, fuse_k2=bool(args.fuse_k2), trait_rank=trait_rank)
         ser.state.copy_(eng.state)
         ser.attach()
         return eng, ser, info
@@ -368,6 +368,30 @@ def run_ours(args):
             engc.close()
             serc.close()
 
+    # ================= low-rank trait weights (reading L1), FP64 and int8-sliced, many traits =================
+    lr_modes, lr_res = {}, []
+    if t >= 16 and args.lowrank_alt:
+        for i8 in (0, 8):
+            engl, serl, setupl = make_engine(i8, True, "eig", trait_rank=-1)
+            rk = engl.trait_rank() if rank == 0 else (None, None, None)
+            for _ in range(args.warmup):
+                engl.run(xr_dev, out=out)
+            msl = max_over_ranks(_timed_steps(engl, xr_dev, out, args.steps, engl.compute_stream, barrier), world,
+                                 dev)
+            ktl = _kernel_pass(serl, xr_dev, out, args.kernel_steps, barrier)
+            kms = {k: ktl[k]["ms"] / args.kernel_steps for k in ("K1", "K2", "K3")}
+            tot = sum(kms.values())
+            lr_modes["lowrank_int8_sliced" if i8 else "lowrank_fp64"] = {
+                "value": pairs_total * args.steps / (msl / 1e3), "unit": UNIT, "ms_per_step": msl / args.steps,
+                "trait_rank": rk[0], "sigma_ratio_dropped": (rk[2] / rk[1]) if rk[1] else None,
+                "share_of_serial_step": {k: v / tot for k, v in kms.items()},
+                "K2_note": "K2 = products against U_r (p r + t + r columns) + the K = r recombination", "setup": setupl}
+            if args.check and rank == 0:
+                torch.cuda.synchronize(dev)
+                lr_res.append((out[0].cpu().numpy(), out[1].cpu().numpy(), out[2].cpu().numpy()))
+            engl.close()
+            serl.close()
+
     # ================= variance-component estimation (the paper's first step, NEXT-3) =================
     est_mode = None
     if args.est_alt and rank == 0:
@@ -376,13 +400,13 @@ def run_ours(args):
     # ---------------- parity spot check on this run's outputs (outside timed regions)
     parity = None
     if args.check and rank == 0:
-        parity = spot_check(cfg, gcfg, ds, lo, hi, [res_fp64] + ([alt_res] if alt is not None else []) + chol_res,
-                            args.check)
+        parity = spot_check(cfg, gcfg, ds, lo, hi,
+                            [res_fp64] + ([alt_res] if alt is not None else []) + chol_res + lr_res, args.check)
         extra = parity.pop("extra")
         if alt is not None:
             alt["parity"] = extra.pop(0)
-        for name, pr in zip(list(chol_modes), extra):
-            chol_modes[name]["parity"] = pr
+        for name, pr in zip(list(chol_modes) + list(lr_modes), extra):
+            (chol_modes if name in chol_modes else lr_modes)[name]["parity"] = pr
 
     res = None
     if rank == 0:
@@ -415,9 +439,10 @@ def run_ours(args):
             "setup": {**setup, "datagen_s": t_gen},
             "clocks": clocks,
         }
-        if alt is not None or chol_modes or est_mode:
+        if alt is not None or chol_modes or est_mode or lr_modes:
             res["modes"] = ({"int8_sliced": alt} if alt is not None else {})
             res["modes"].update(chol_modes)
+            res["modes"].update(lr_modes)
             if est_mode:
                 res["modes"]["estimate"] = est_mode
         if parity is not None:
@@ -552,6 +577,8 @@ def main(argv=None):
                     help="skip the CLAK-Chol (Alg. 3) modes reported under `modes` for single-trait configs")
     ap.add_argument("--no-int8-alt", dest="int8_alt", action="store_false",
                     help="skip the int8-sliced mode measurement reported under `modes`")
+    ap.add_argument("--no-lowrank-alt", dest="lowrank_alt", action="store_false",
+                    help="skip the low-rank trait-weight modes (reading L1) reported under `modes` for t >= 16")
     ap.add_argument("--no-est-alt", dest="est_alt", action="store_false",
                     help="skip the variance-component estimation measurement reported under `modes.estimate`")
     ap.add_argument("--e2e-steps", type=int, default=2)
