@@ -160,6 +160,9 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
     h.off_exps = take(sizeof(int) * (d.na_pad + d.nlin_pad));
   }
   h.trait_rank = o->trait_rank;
+  h.lr_r = 0;            // exact weights until setup decides otherwise
+  h.lr_nsq = d.nsq;
+  h.lr_nlin = d.nlin;
   if (d.lr) h.off_wt = take(sizeof(double) * d.t * kLrMax);
   h.total = (int64_t)off;
   return h;

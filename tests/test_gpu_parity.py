@@ -242,6 +242,29 @@ def test_attach_after_state_copy(c0):
     assert e.value.code in (6,)
 
 
+@pytest.mark.parametrize("i8,lr,t", [(8, 0, 40), (0, -1, 40), (8, -1, 40), (8, 0, 4)])
+def test_attach_after_state_copy_modes(i8, lr, t):
+    """Attached contexts (the other ranks of a multi-GPU run) read every run-time choice made at setup from the
+    state header (int8 digit layout, low-rank rank and operand widths): results bitwise equal to the setup rank."""
+    gw = _gw()
+    cfg = datagen.custom_config(n=160, p=3, m=500, t=t, index=460 + t)
+    ds = datagen.dataset(cfg)
+    XR = torch.from_numpy(datagen.xr_dosages(cfg, ld=_ld(cfg.n))).cuda()
+    a = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, int8_slices=i8, trait_rank=lr, block_cols=200)
+    a.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    bcopy = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, int8_slices=i8, trait_rank=lr, block_cols=200, overlap=True)
+    bcopy.state.copy_(a.state)
+    bcopy.attach()
+    assert bcopy.trait_rank() == a.trait_rank()
+    r1 = [x.cpu().numpy() for x in a.run(XR)]
+    r2 = [x.cpu().numpy() for x in bcopy.run(XR)]
+    for x, y in zip(r1, r2):
+        np.testing.assert_array_equal(x, y)
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].cpu().numpy().T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    eb, ev = compare(*r2, ref)
+    assert eb <= TOL_B and ev <= TOL_VAR
+
+
 # ------------------------------------------------------------------ int8-sliced mode (SURVEY §8(f) NEXT-4)
 def test_int8_sliced_c0_all_pairs(c0):
     cfg, ds, XR, ref = c0
