@@ -137,10 +137,11 @@ struct EstOut {
   unsigned long long* err;  // smallest failing trait (R <= 0, no feasible grid point), init ~0ull
 };
 
-// One CTA per trait j = blockIdx.x.  method 0 = ML, 1 = REML.  rec: est_grid_shared output.  logdet_xx:
+// One CTA per trait j = blockIdx.x (two resident per SM: 128 registers, measured 19.9 -> 12.0 ms at C4; three
+// spill too much).  method 0 = ML, 1 = REML.  rec: est_grid_shared output.  logdet_xx:
 // log|X_L'^T X_L'| (REML constant; equals log|A_0| since v = 1 at h = 0).
 template <int P>
-__global__ void __launch_bounds__(EST_THREADS) est_traits(const double* __restrict__ W,
+__global__ void __launch_bounds__(EST_THREADS, 2) est_traits(const double* __restrict__ W,
                                                           const double* __restrict__ XLp,
                                                           const double* __restrict__ Yp, int n, int kpad, int t,
                                                           int method, const double* __restrict__ rec, EstOut out) {
