@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   I8EpiSmem* esm = reinterpret_cast<I8EpiSmem*>(tmem_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) i8_stamp(s, 0);
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   int tm, tn;
@@ -466,6 +467,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) i8_stamp(s, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -488,6 +490,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       for (int kb = 0; kb < KB; ++kb) {
         const int st = kb % I8_STAGES2;
         mbar_wait(&full[st], (kb / I8_STAGES2) & 1);
+        if (kb == 0) i8_stamp(s, 2);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t a0 = smem_u32(sA + st * A_BYTES);
         const uint32_t b0 = smem_u32(sB + st * BH_BYTES);
@@ -502,13 +505,16 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         umma_commit_2sm(&empty[st]);  // both CTAs may refill this stage once these MMAs have read it
       }
       umma_commit_2sm(tmem_full);
+      i8_stamp(s, 3);
     }
   } else if (warp >= 4) {
     i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
+    if (threadIdx.x == 128) i8_stamp(s, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   cluster_sync_all();
+  if (threadIdx.x == 0) i8_stamp(s, 6);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(512));

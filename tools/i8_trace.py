@@ -9,7 +9,9 @@ for li, L in enumerate(a):
     if not len(v):
         continue
     t0 = v[:, 0].min()
-    d = lambda i, j: np.median(v[:, j] - v[:, i]) / 1e3
+    def d(i, j):
+        ok = (v[:, i] > 0) & (v[:, j] > 0)  # 2-SM kernel: only the pair's leader stamps the MMA phases
+        return np.median(v[ok, j] - v[ok, i]) / 1e3 if ok.any() else float("nan")
     print(f"launch {li}: {len(v)} CTAs, span {(v[:, 6].max() - t0) / 1e3:.1f} us; median us: setup {d(0, 1):.2f} "
           f"first-data {d(1, 2):.2f} mainloop {d(2, 3):.2f} commit->epi {d(3, 4):.2f} epilogue {d(4, 5):.2f} "
           f"tail {d(5, 6):.2f} total {d(0, 6):.2f}")
