@@ -317,7 +317,8 @@ def run_ours(args):
     # ================= int8-sliced mode, same inputs =================
     alt = None
     if args.int8_alt:
-        eng8, ser8, setup8 = make_engine(8, True)
+        S = args.int8_slices
+        eng8, ser8, setup8 = make_engine(S, True)
         for _ in range(args.warmup):
             eng8.run(xr_dev, out=out)
         ms8 = max_over_ranks(_timed_steps(eng8, xr_dev, out, args.steps, eng8.compute_stream, barrier), world, dev)
@@ -326,11 +327,13 @@ def run_ours(args):
         i1_ms, i2_ms, i3_ms = (kt8[k]["ms"] / args.kernel_steps for k in ("K1", "K2", "K3"))
         na_pad = (n + 63) // 64 * 64
         nlin_pad = (t * (p + 1) + 63) // 64 * 64
-        i8_ops = sum(2.0 * c * (na_pad + nlin_pad) * 8 * n for c in blocks)   # int8 MACs x 2 actually issued
+        i8_ops = sum(2.0 * c * (na_pad + nlin_pad) * S * n for c in blocks)   # int8 MACs x 2 actually issued
         i8_peak = 2.0 * 1623.7  # MEASURED_PEAKS bf16 x the nominal int8/bf16 ratio (4.5 / 2.25)
         k2b_flops = sum(2.0 * n * c * t for c in blocks)
         alt = {"value": value8, "unit": UNIT, "ms_per_step": ms8 / args.steps,
-               "roofline": {"bound": "tensor", "kernel": "K1i+K2a int8-sliced tcgen05 (8 digits, TMEM int32)",
+               "int8_slices": S,
+               "representation_error": f"<= 2^-{7 * S + 1} of each digitised column's largest entry",
+               "roofline": {"bound": "tensor", "kernel": f"K1i+K2a int8-sliced tcgen05 ({S} digits, TMEM int32)",
                             "achieved": i8_ops / (i1_ms / 1e3) / 1e12, "peak": i8_peak, "unit": "TOPS",
                             "frac": i8_ops / (i1_ms / 1e3) / 1e12 / i8_peak,
                             "peak_source": "MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8/bf16 ratio)",
@@ -350,7 +353,7 @@ def run_ours(args):
     # ================= CLAK-Chol single-trait path (Alg. 3, NEXT-1), t == 1 only =================
     chol_modes, chol_res = {}, []
     if t == 1 and args.chol_alt:
-        for i8 in (0, 8):
+        for i8 in (0, args.int8_slices):
             engc, serc, setupc = make_engine(i8, True, "chol")
             for _ in range(args.warmup):
                 engc.run(xr_dev, out=out)
@@ -374,7 +377,7 @@ def run_ours(args):
     # ================= low-rank trait weights (reading L1), FP64 and int8-sliced, many traits =================
     lr_modes, lr_res = {}, []
     if t >= 16 and args.lowrank_alt:
-        for i8 in (0, 8):
+        for i8 in (0, args.int8_slices):
             engl, serl, setupl = make_engine(i8, True, "eig", trait_rank=-1)
             rk = engl.trait_rank() if rank == 0 else (None, None, None)
             for _ in range(args.warmup):
@@ -582,6 +585,8 @@ def main(argv=None):
     ap.add_argument("--kernel-steps", type=int, default=1, help="serial passes timed per kernel (roofline)")
     ap.add_argument("--no-chol-alt", dest="chol_alt", action="store_false",
                     help="skip the CLAK-Chol (Alg. 3) modes reported under `modes` for single-trait configs")
+    ap.add_argument("--int8-slices", type=int, default=7, choices=(7, 8),
+                    help="digits per fp64 value in the int8-sliced modes (8: <= 2^-57 representation error, 7: 2^-50)")
     ap.add_argument("--no-int8-alt", dest="int8_alt", action="store_false",
                     help="skip the int8-sliced mode measurement reported under `modes`")
     ap.add_argument("--no-lowrank-alt", dest="lowrank_alt", action="store_false",

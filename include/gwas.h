@@ -76,11 +76,13 @@ typedef struct {
   void* compute_stream;    /* cudaStream_t for kernels (NULL = legacy default stream) */
   void* copy_stream;       /* cudaStream_t for host->HBM staging of X_R blocks (NULL = compute_stream) */
   int32_t timing;          /* 1 = bracket every K1/K2/K3/H2D launch with CUDA events (gwas_kernel_times) */
-  int32_t int8_slices;     /* 0 (default): K1/K2 on the FP64 DMMA tensor pipe.  8: exact integer-sliced mode
+  int32_t int8_slices;     /* 0 (default): K1/K2 on the FP64 DMMA tensor pipe.  8 or 7: integer-sliced mode
                               (requires xr_dtype = GWAS_XR_U8 and n <= 66000): X_R^T Z and
                               the linear K2 terms X_R^T (Z D_j [X_L' | y'_j]) run as int8 tcgen05 products against
-                              8 signed digits of each fp64 column (exact int32 accumulation in TMEM), the
-                              W_R^T W_R term stays on DMMA.  Fixed at setup (part of the state). */
+                              S signed digits of each fp64 column (exact int32 accumulation in TMEM), the
+                              W_R^T W_R term stays on DMMA.  Representation error of a column: <= 2^-57 (S = 8, below
+                              fp64 rounding) or 2^-50 (S = 7, 12 % less tensor work; below the error of Z itself)
+                              of its largest entry.  Fixed at setup (part of the state). */
   int32_t overlap;         /* 1 = pipeline blocks over two streams: block b's K2 + K3 run on an internal auxiliary
                               stream while block b+1's K1 runs on compute_stream (double-buffered intermediates;
                               the stream is created and owned by the context).  gwas_run still completes on

@@ -29,13 +29,25 @@
 
 namespace gw {
 
-constexpr int I8_SLICES = 8;       // digits per fp64 value
+constexpr int I8_SLICES = 8;       // digits per fp64 value of the exact variant (the 2-SM kernel supports only this)
 constexpr int I8_NB = 64;          // output columns per tile
 constexpr int I8_BM = 128;         // output rows (SNPs) per tile
 constexpr int I8_BKB = 64;         // K bytes per stage (64-byte swizzle atom rows)
 constexpr int I8_STAGES = 5;
 constexpr int I8_THREADS = 256;
 constexpr int I8_BROWS = I8_SLICES * I8_NB;  // 512 B rows per tile = TMEM columns
+
+// Per digit count S (int8_slices = 7 or 8): B rows per tile (S x 64, TMEM columns of the accumulators) and the
+// stage ring depth that fits 227 KB of shared memory (A 8 KB + B S x 4 KB per 64-byte K stage).
+template <int S>
+struct I8Cfg {
+  static_assert(S == 7 || S == 8, "int8_slices must be 7 or 8");
+  static constexpr int BROWS = S * I8_NB;
+  static constexpr int STAGES = S == 8 ? 5 : 6;
+  static constexpr size_t smem_bytes(size_t epi) {
+    return 1024 + (size_t)STAGES * (I8_BM + BROWS) * I8_BKB + 256 + epi;
+  }
+};
 
 struct I8Shape {
   int M;              // rows of A (SNPs of the block)
@@ -158,6 +170,7 @@ struct I8EpiSmem {
 };
 constexpr int I8_EPI_SMEM = (int)sizeof(I8EpiSmem);
 
+template <int S>
 __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base, uint64_t* tmem_full, int m0, int tn,
                                             int warp, int lane, I8EpiSmem* es) {
   // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = tile rows
@@ -188,28 +201,30 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
   for (int j0 = 0; j0 < I8_NB; j0 += EPI_CW) {
     // all S digit planes of EPI_CW columns in flight at once, one wait (the drain is otherwise a chain of S
     // dependent TMEM round trips per chunk, exposed because the accumulators fill TMEM and nothing overlaps them)
-    int32_t v[I8_SLICES][EPI_CW];
+    int32_t v[S][EPI_CW];
     if (s.dbg != 1) {
 #pragma unroll
-      for (int sl = 0; sl < I8_SLICES; ++sl) tmem_ld8(tl + sl * I8_NB + j0, v[sl]);
+      for (int sl = 0; sl < S; ++sl) tmem_ld8(tl + sl * I8_NB + j0, v[sl]);
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     } else {
 #pragma unroll
-      for (int sl = 0; sl < I8_SLICES; ++sl)
+      for (int sl = 0; sl < S; ++sl)
 #pragma unroll
         for (int c = 0; c < EPI_CW; ++c) v[sl][c] = lane + sl + c + j0;
     }
-    // exact integer recombination of the digit accumulators in two 4-digit halves (|.| < 2^53 each, so both
+    // exact integer recombination of the digit accumulators in two halves of <= 4 digits (|.| < 2^53 each, so both
     // convert exactly), one fp64 rounding (the fma), then the exact power-of-two column scale 2^(e - 28):
-    //   x = sum_s I_s 2^(-7(s+1)) 2^e = (hi + lo 2^-28) 2^(e - 28),  hi = sum_{s<4} I_s 2^(7(3-s)),
-    //   lo = sum_{s>=4} I_s 2^(7(7-s))
-    static_assert(I8_SLICES == 8, "two 4-digit halves");
+    //   x = sum_s I_s 2^(-7(s+1)) 2^e = (hi + lo 2^(-7(S-4))) 2^(e - 28),  hi = sum_{s<4} I_s 2^(7(3-s)),
+    //   lo = sum_{4<=s<S} I_s 2^(7(S-1-s))
+    constexpr double lo_scale = S == 8 ? 0x1p-28 : 0x1p-21;
     double acc[EPI_CW];
 #pragma unroll
     for (int c = 0; c < EPI_CW; ++c) {
       const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 + v[3][c];
-      const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 + v[7][c];
-      acc[c] = fma((double)lo, 0x1p-28, (double)hi) * es->scale[j0 + c];
+      long long lo = v[4][c];
+#pragma unroll
+      for (int sl = 5; sl < S; ++sl) lo = lo * 128 + v[sl][c];
+      acc[c] = fma((double)lo, lo_scale, (double)hi) * es->scale[j0 + c];
     }
     if (fuse) {
 #pragma unroll
@@ -257,11 +272,13 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
 // column tile, and each loads 1/CL of the shared digit slab and multicasts it to all (L2 reads of the dominant
 // B operand / CL).  Stage slots are released cluster-wide: every CTA's MMA completion arrives on every CTA's
 // empty barrier (count CL).
-template <int CL>
+template <int CL, int S>
 __global__ void __launch_bounds__(I8_THREADS, 1)
     gemm_i8_sliced(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Shape s) {
+  constexpr int I8_STAGES = I8Cfg<S>::STAGES;
+  constexpr int BROWS = I8Cfg<S>::BROWS;       // S x 64
   constexpr int A_BYTES = I8_BM * I8_BKB;      // 8 KB
-  constexpr int B_BYTES = I8_BROWS * I8_BKB;   // 32 KB
+  constexpr int B_BYTES = BROWS * I8_BKB;      // S x 4 KB
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -290,7 +307,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     tn = r / gsz;
   }
   const int m0 = tm * I8_BM;
-  const int brow0 = tn * I8_BROWS;
+  const int brow0 = tn * BROWS;
   const int k_end = tn < s.tri_tiles ? min(s.K, (tn + 1) * I8_NB) : s.K;
   const int KB = (k_end + I8_BKB - 1) / I8_BKB;
 
@@ -323,11 +340,11 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         if (kb >= I8_STAGES) mbar_wait(&empty[st], ((kb / I8_STAGES) - 1) & 1);
         mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
         tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * I8_BKB, m0);
-        if constexpr (CL == 1) {
+        if constexpr (CL == 1) {  // two boxes of BROWS/2 rows (the tensor map's box)
           tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * I8_BKB, brow0);
-          tma_load_2d(sB + st * B_BYTES + 256 * I8_BKB, &tmB, &full[st], kb * I8_BKB, brow0 + 256);
+          tma_load_2d(sB + st * B_BYTES + (BROWS / 2) * I8_BKB, &tmB, &full[st], kb * I8_BKB, brow0 + BROWS / 2);
         } else {
-          constexpr int QR = I8_BROWS / CL;  // rows of the slab this CTA fetches for the whole cluster
+          constexpr int QR = BROWS / CL;  // rows of the slab this CTA fetches for the whole cluster
           tma_load_2d_mc(sB + st * B_BYTES + crank * QR * I8_BKB, &tmB, &full[st], kb * I8_BKB,
                          brow0 + (int)crank * QR, (uint16_t)((1u << CL) - 1));
         }
@@ -335,7 +352,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(256);
+      constexpr uint32_t idesc = idesc_i8(256);               // digits 0..3 of the tile's 64 columns
+      constexpr uint32_t idesc2 = idesc_i8((S - 4) * I8_NB);  // digits 4..S-1
       for (int kb = 0; kb < KB; ++kb) {
         const int st = kb % I8_STAGES;
         mbar_wait(&full[st], (kb / I8_STAGES) & 1);
@@ -350,7 +368,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
           const uint64_t bd1 = umma_desc_sw64(b0 + 256 * I8_BKB + kk * 32);
           const uint32_t acc = (kb | kk) ? 1u : 0u;
           umma_i8(tmem_base, ad, bd0, idesc, acc);
-          umma_i8(tmem_base + 256, ad, bd1, idesc, acc);
+          umma_i8(tmem_base + 256, ad, bd1, idesc2, acc);
         }
         // frees the smem slot (in every CTA of the cluster) when these MMAs have read it
         if constexpr (CL == 1) umma_commit(&empty[st]);
@@ -360,7 +378,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       i8_stamp(s, 3);
     }
   } else if (warp >= 4) {
-    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
+    i8_epilogue<S>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
     if (threadIdx.x == 128) i8_stamp(s, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -508,7 +526,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       i8_stamp(s, 3);
     }
   } else if (warp >= 4) {
-    i8_epilogue(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
+    i8_epilogue<I8_SLICES>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
     if (threadIdx.x == 128) i8_stamp(s, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -528,7 +546,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
 // Row `r` (an output column of the product) goes to digit rows dst_row(r, s) = (r / 64) * 512 + s * 64 + r % 64
 // of D (ldd bytes per row, pad zero); exps[r] = e with |X[r, :]| 2^-e <= 127/128.  One CTA per row.
 __global__ void digitize_rows(const double* __restrict__ X, long long ldx, int rows, int n, int row_off,
-                              int8_t* __restrict__ D, long long ldd, int* __restrict__ exps) {
+                              int8_t* __restrict__ D, long long ldd, int* __restrict__ exps, int S) {
   const int r = blockIdx.x;
   if (r >= rows) return;
   const double* x = X + (long long)r * ldx;
@@ -553,11 +571,10 @@ __global__ void digitize_rows(const double* __restrict__ X, long long ldx, int r
   }
   const int gr = r + row_off;
   if (threadIdx.x == 0) exps[gr] = e;
-  const long long base = (long long)(gr / I8_NB) * I8_BROWS + gr % I8_NB;
+  const long long base = (long long)(gr / I8_NB) * (S * I8_NB) + gr % I8_NB;
   for (int k = threadIdx.x; k < ldd; k += blockDim.x) {
     double v = k < n ? ldexp(x[k], -e + 7) : 0.0;  // |v| <= 127
-#pragma unroll
-    for (int sl = 0; sl < I8_SLICES; ++sl) {
+    for (int sl = 0; sl < S; ++sl) {
       const double d = rint(v);
       D[(base + (long long)sl * I8_NB) * ldd + k] = (int8_t)d;
       v = (v - d) * 128.0;  // exact: |v - d| <= 1/2

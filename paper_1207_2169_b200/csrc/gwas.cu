@@ -156,7 +156,7 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
   h.nlin = d.nlin;
   h.nlin_pad = d.nlin_pad;
   if (d.i8) {
-    h.off_dig = take((size_t)((d.na_pad + d.nlin_pad) / gw::I8_NB) * gw::I8_BROWS * d.kpad);
+    h.off_dig = take((size_t)((d.na_pad + d.nlin_pad) / gw::I8_NB) * o->int8_slices * gw::I8_NB * d.kpad);
     h.off_exps = take(sizeof(int) * (d.na_pad + d.nlin_pad));
   }
   h.trait_rank = o->trait_rank;
@@ -269,8 +269,8 @@ gwas_status check_sizes(int64_t n, int64_t p, int64_t t, const gwas_options* o) 
   if (o->algorithm == GWAS_ALG_CHOL && t != 1)
     return fail(GWAS_E_ARG, "CLAK-Chol (Alg. 3) is the single-trait algorithm: t = %lld != 1", (long long)t);
   if (o->int8_slices != 0) {
-    if (o->int8_slices != gw::I8_SLICES)
-      return fail(GWAS_E_ARG, "int8_slices = %d unsupported (0 or %d)", o->int8_slices, gw::I8_SLICES);
+    if (o->int8_slices != 7 && o->int8_slices != 8)
+      return fail(GWAS_E_ARG, "int8_slices = %d unsupported (0, 7 or 8)", o->int8_slices);
     if (o->xr_dtype != GWAS_XR_U8) return fail(GWAS_E_ARG, "int8-sliced mode needs uint8 X_R (exact dosages)");
     if (n > 66000) return fail(GWAS_E_ARG, "int8-sliced mode: n = %lld > 66000 (int32 accumulator bound)", (long long)n);
   }
@@ -508,12 +508,47 @@ gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
 }
 
 // K1i/K2a: C_a[i][c] (c < na) and C_b[i][c'] (c' < nb) from the u8 A block and the stacked digit matrix.
-gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const int8_t* dig, int64_t ldd,
+// Launch of the S-digit kernel with cluster size CL (1 = plain launch).
+template <int S>
+gwas_status launch_i8_s(int CL, const CUtensorMap& ma, const CUtensorMap& mb, const gw::I8Shape& s, unsigned grid,
+                        cudaStream_t st) {
+  constexpr size_t smem = gw::I8Cfg<S>::smem_bytes(gw::I8_EPI_SMEM);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<1, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<2, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<4, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  if (CL == 1) {
+    gw::gemm_i8_sliced<1, S><<<grid, gw::I8_THREADS, smem, st>>>(ma, mb, s);
+    CKC(cudaGetLastError());
+    return GWAS_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(gw::I8_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (CL == 2) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<2, S>, ma, mb, s));
+  else CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4, S>, ma, mb, s));
+  return GWAS_OK;
+}
+
+gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, const int8_t* dig, int64_t ldd,
                       int64_t tiles_n, int64_t na_tiles, const int* exps, double* Ca, int64_t ldca, int64_t na,
                       double* Cb, int64_t ldcb, int64_t nb, cudaStream_t st, int64_t tri_tiles = 0,
                       int ft = 0, const double* fD = nullptr, int64_t fld = 0, double* fP = nullptr,
                       int64_t fP_stride = 0) {
   if (M <= 0) return GWAS_OK;
+  if (S != 7 && S != 8) return fail(GWAS_E_ARG, "int8 digits %d", S);
   // GWAS_I8_KERNEL: "1sm" (default) with GWAS_I8_CLUSTER (1, 2 or 4; default 2) CTAs multicasting the digit
   // slab, or "2sm" (CTA pairs with cta_group::2 MMAs).  Measured at C4 per 8192-column block: 1sm x1 14.4 ms,
   // x2 8.8 ms, x4 9.9 ms; 2sm 9.4 ms.
@@ -526,12 +561,13 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
     const int v = e ? atoi(e) : 2;
     return (v == 1 || v == 2 || v == 4) ? v : 2;
   }();
-  const bool two_sm = mode_env == 2 && M > gw::I8_BM;
+  const bool two_sm = mode_env == 2 && M > gw::I8_BM && S == gw::I8_SLICES;
   const int CL = two_sm ? 2 : ((M >= (int64_t)cl_env * gw::I8_BM) ? cl_env : 1);
+  const int brows = S * gw::I8_NB;  // digit rows per 64-column tile
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, true, K, M, lda, gw::I8_BM, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
-  const int box_b = two_sm ? 128 : (CL == 1 ? 256 : gw::I8_BROWS / CL);
-  CKG(make_map(&mb, dig, true, K, tiles_n * gw::I8_BROWS, ldd, box_b, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
+  const int box_b = two_sm ? 128 : (CL == 1 ? brows / 2 : brows / CL);
+  CKG(make_map(&mb, dig, true, K, tiles_n * brows, ldd, box_b, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
   gw::I8Shape s;
   s.M = (int)M;
   s.K = (int)K;
@@ -562,35 +598,32 @@ gwas_status launch_i8(const void* A, int64_t lda, int64_t M, int64_t K, const in
   s.fld = fld;
   s.fP = fP;
   s.fP_stride = fP_stride;
-  constexpr size_t smem = 1024 + gw::I8_STAGES * (gw::I8_BM + gw::I8_BROWS) * gw::I8_BKB + 256 + gw::I8_EPI_SMEM;
-  constexpr size_t smem2 = 1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256 + gw::I8_EPI_SMEM;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
   const unsigned grid = (unsigned)(s.tiles_m * s.tiles_n);
-  if (CL == 1) {
-    gw::gemm_i8_sliced<1><<<grid, gw::I8_THREADS, smem, st>>>(ma, mb, s);
-  } else {
+  if (two_sm) {
+    constexpr size_t smem2 =
+        1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256 + gw::I8_EPI_SMEM;
+    static bool attr2 = false;
+    if (!attr2) {
+      CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      attr2 = true;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(gw::I8_THREADS);
-    cfg.dynamicSmemBytes = two_sm ? smem2 : smem;
+    cfg.dynamicSmemBytes = smem2;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (two_sm) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced_2sm, ma, mb, s));
-    else if (CL == 2) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<2>, ma, mb, s));
-    else CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4>, ma, mb, s));
+    CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced_2sm, ma, mb, s));
+  } else if (S == 8) {
+    CKG(launch_i8_s<8>(CL, ma, mb, s, grid, st));
+  } else {
+    CKG(launch_i8_s<7>(CL, ma, mb, s, grid, st));
   }
   CKC(cudaGetLastError());
   if (trace_dev) {
@@ -1030,13 +1063,14 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
           c->Z(), zt, (int)d.kpad);
       CKC(cudaGetLastError());
       CKG(gemm_tn(false, c->B2(), d.kpad, zt, d.kpad, blin, d.kpad, nlin_eff, n, n, n, cs));
-      const size_t dig_bytes = (size_t)((d.na_pad + nlin_pad_eff) / gw::I8_NB) * gw::I8_BROWS * d.kpad;
+      const size_t dig_bytes = (size_t)((d.na_pad + nlin_pad_eff) / gw::I8_NB) * o->int8_slices * gw::I8_NB * d.kpad;
       CKC(cudaMemsetAsync(c->dig(), 0, dig_bytes, cs));
       CKC(cudaMemsetAsync(c->exps(), 0, sizeof(int) * (d.na_pad + nlin_pad_eff), cs));
-      gw::digitize_rows<<<(unsigned)n, 256, 0, cs>>>(c->Z(), d.kpad, (int)n, (int)n, 0, c->dig(), d.kpad, c->exps());
+      gw::digitize_rows<<<(unsigned)n, 256, 0, cs>>>(c->Z(), d.kpad, (int)n, (int)n, 0, c->dig(), d.kpad, c->exps(),
+                                                     o->int8_slices);
       CKC(cudaGetLastError());
       gw::digitize_rows<<<(unsigned)nlin_eff, 256, 0, cs>>>(blin, d.kpad, (int)nlin_eff, (int)n, (int)d.na_pad,
-                                                             c->dig(), d.kpad, c->exps());
+                                                             c->dig(), d.kpad, c->exps(), o->int8_slices);
       CKC(cudaGetLastError());
     }
     CKC(cudaEventRecord(e3, cs));
@@ -1260,7 +1294,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     } else {
       // K1i + K2a (int8-sliced, exact): X_R'^T = X_R^T Z and C[:, 0:t(p+1)] = X_R^T (Z B_op) in one launch
       CKG(c->tic(GWAS_K1, cs, &dummy));
-      CKG(launch_i8(A, lda, cols, d.n, c->dig(), d.kpad, (d.na_pad + round_up(lr_nlin, gw::I8_NB)) / gw::I8_NB,
+      CKG(launch_i8(c->opt.int8_slices, A, lda, cols, d.n, c->dig(), d.kpad, (d.na_pad + round_up(lr_nlin, gw::I8_NB)) / gw::I8_NB,
                     d.na_pad / gw::I8_NB, c->exps(), xrp, d.kpad, d.n, lr_r > 0 ? g2 : c2,
                     lr_r > 0 ? d.ldg2 : d.ldc2, lr_nlin, cs, chol ? d.na_pad / gw::I8_NB : 0,
                     d.fuse ? (int)d.t : 0, c->B2() + d.nsq * d.kpad, d.kpad, fpart, fstride));
