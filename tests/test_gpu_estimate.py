@@ -158,3 +158,23 @@ def test_estimate_errors():
     with pytest.raises(gw.GwasError):
         ch.setup_estimate(ds.Phi, ds.XL, ds.Y[:, :1], "ml")
     ch.close()
+
+
+def test_estimate_with_lowrank_weights_and_int8():
+    """Estimation feeds the low-rank weight factorisation and the int8-sliced run the same way as given (h2, s2)."""
+    cfg = datagen.custom_config(n=240, p=4, m=500, t=48, index=0)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    eng, est = _estimate(cfg, ds, "reml", block_cols=256, trait_rank=-1, int8_slices=7)
+    assert eng.trait_rank()[0] > 0
+    b, v, s = eng.run(torch.from_numpy(XR).cuda())
+    torch.cuda.synchronize()
+    b, v, s = b.cpu().numpy(), v.cpu().numpy(), s.cpu().numpy()
+    eng.close()
+    ref_est = _oracle_estimate(ds, "reml", np.arange(cfg.t))
+    eh, es, el = _check(ds, "reml", est, ref_est, np.arange(cfg.t))
+    assert eh <= TOL_H2 and es <= TOL_S2 and el <= TOL_LL
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ref_est["h2"],
+                              ref_est["sigma2"])
+    eb, ev = compare(b, v, s, ref)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
