@@ -404,7 +404,14 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
     return e ? atoi(e) : 4;
   }();
   const int64_t tiles128 = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
-  const int bn = (N <= 64 || tiles128 < (int64_t)bn64_waves * 148) ? 64 : 128;
+  int bn = (N <= 64 || tiles128 < (int64_t)bn64_waves * 148) ? 64 : 128;
+  if (!a_u8 && N > 64 && !getenv("GWAS_BN64_WAVES")) {
+    // fp64 A (one CTA per SM either way): compare whole waves, a 64-wide tile doing half the work of a 128-wide
+    // one at ~93 % of its efficiency (measured on K2b, C4: 5.36 ms at 128 vs 5.04 ms at 64 wide)
+    const int64_t tiles64 = ((M + kBM - 1) / kBM) * ((N + 63) / 64);
+    const double cost128 = (double)((tiles128 + 147) / 148), cost64 = (double)((tiles64 + 147) / 148) * 0.5 / 0.93;
+    bn = cost64 < cost128 ? 64 : 128;
+  }
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, a_u8, K, M, lda, kBM));
   CKG(make_map(&mb, B, false, K, N, ldb, bn));
