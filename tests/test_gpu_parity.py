@@ -521,3 +521,49 @@ def test_lowrank_skipped_for_few_traits():
     eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
     assert eng.trait_rank()[0] == 0
     eng.close()
+
+
+# ------------------------------------------------------------------ maximum sizes and degenerate cases
+@pytest.mark.parametrize("i8,mode", [(0, "full"), (7, "full"), (8, "snp")])
+def test_max_covariates_p12(i8, mode):
+    """p = 12 (the largest X_L width the kernels are instantiated for), ragged n, several blocks."""
+    cfg = datagen.custom_config(n=301, p=12, m=520, t=9, index=470)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), int8_slices=i8, output_mode=mode, block_cols=200)
+    eb, ev = compare(b, v, s, ref, full=mode == "full")
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+def test_degenerate_h2_zero_and_identity_kinship():
+    """h2 = 0 (M = sigma2 I for any Phi) and Phi = I (M = sigma2 I for any h2): the GLS reduces to OLS.  Checked
+    against numpy lstsq (independent of both the oracle and the GPU path), plus the oracle."""
+    cfg = datagen.custom_config(n=150, p=3, m=200, t=4, index=471)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    G = XR[:, :cfg.n].T.astype(np.float64)
+    for Phi, h2 in ((ds.Phi, np.zeros(cfg.t)), (np.eye(cfg.n), ds.h2)):
+        b, v, s = _run(cfg, datagen.Dataset(cfg, Phi, ds.XL, ds.Y, h2, ds.s2), torch.from_numpy(XR).cuda())
+        for j in range(cfg.t):
+            for i in (0, 57, cfg.m - 1):
+                X = np.column_stack([ds.XL, G[:, i]])
+                beta, res, *_ = np.linalg.lstsq(X, ds.Y[:, j], rcond=None)
+                var_g = np.linalg.inv(X.T @ X)[-1, -1] * ds.s2[j]   # Var = (X^T M^-1 X)^-1 with M = s2 I
+                assert abs(b[i, j] - beta[-1]) <= 1e-9 * np.sqrt(var_g)
+                assert abs(v[i, j] - var_g) <= 1e-9 * var_g
+        ref = oracle.gls_sequence(Phi, ds.XL, G, ds.Y, h2, ds.s2)
+        eb, ev = compare(b, v, s, ref)
+        assert eb <= TOL_B and ev <= TOL_VAR
+
+
+def test_sigma2_scaling_on_gpu():
+    """sigma2 -> alpha sigma2: b unchanged, Var x alpha (textbook convention, reading A1); bitwise-close."""
+    cfg = datagen.custom_config(n=180, p=4, m=300, t=5, index=472)
+    ds = datagen.dataset(cfg)
+    XR = torch.from_numpy(datagen.xr_dosages(cfg, ld=_ld(cfg.n))).cuda()
+    b1, v1, s1 = _run(cfg, ds, XR)
+    b2, v2, s2 = _run(cfg, datagen.Dataset(cfg, ds.Phi, ds.XL, ds.Y, ds.h2, 4.0 * ds.s2), XR)
+    np.testing.assert_array_equal(s1, s2)
+    np.testing.assert_allclose(b2, b1, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(v2, 4.0 * v1, rtol=1e-12)
