@@ -31,6 +31,7 @@
  *   GWAS_I8_CLUSTER=1|2|4   int8 kernel cluster size (digit-slab multicast), default 2
  *   GWAS_I8_KERNEL=2sm      the 2-SM (cta_group::2) int8 kernel, 8 digits only (measured slower; not the default)
  *   GWAS_BN64_WAVES=w       force the 128/64-wide tile choice of the DMMA kernel by a w-wave threshold
+ *   GWAS_K1_GROUP=g         K1 rasterisation group (row tiles per sweep of the Z panels), default 32
  *   GWAS_I8_TRACE=<file>    append %globaltimer phase stamps of the int8 kernel to <file> (allocates a 256 KB
  *                           device buffer and synchronises after every launch)
  *   GWAS_I8_DBG=1|2         int8 epilogue without TMEM loads / stores (timing experiments; results invalid) */
