@@ -32,6 +32,8 @@
  *   GWAS_I8_KERNEL=2sm      the 2-SM (cta_group::2) int8 kernel, 8 digits only (measured slower; not the default)
  *   GWAS_BN64_WAVES=w       force the 128/64-wide tile choice of the DMMA kernel by a w-wave threshold
  *   GWAS_K1_GROUP=g         K1 rasterisation group (row tiles per sweep of the Z panels), default 32
+ *   GWAS_K2_GROUP=g         K2 rasterisation group, default 16 (DRAM read per C4 block: 4 -> 10.9, 8 -> 7.9,
+ *                           16 -> 6.8, 32 -> 9.8, 64 -> 17.5 GB; time 32.4-32.6 ms for all: DMMA-bound)
  *   GWAS_I8_TRACE=<file>    append %globaltimer phase stamps of the int8 kernel to <file> (allocates a 256 KB
  *                           device buffer and synchronises after every launch)
  *   GWAS_I8_DBG=1|2         int8 epilogue without TMEM loads / stores (timing experiments; results invalid) */

@@ -1298,7 +1298,9 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
                     splitbuf));
         CKG(lowrank_recombine(c, g2, c2, cols, cs2));
       } else {
-        CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, 16, splitbuf));
+        static const int k2_group = getenv("GWAS_K2_GROUP") ? atoi(getenv("GWAS_K2_GROUP")) : 16;
+        CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, k2_group,
+                    splitbuf));
       }
       CKG(c->toc(cs2));
     } else {
