@@ -108,7 +108,7 @@ typedef struct {
                               choice (not part of the state); results differ from the unfused path only by rounding. */
   int32_t trait_rank;      /* 0 (default): the exact per-trait weights D_j of Alg. 4 line 6 in K2 (the paper's design).
                               -1: low-rank trait weights (reading L1, CLAK-Eig only, t >= 16): setup
-                              factors D = [d_1 .. d_t] = U S V^T (cuSOLVER gesvd), keeps the r <= 64 singular
+                              factors D = [d_1 .. d_t] = U S V^T (cuSOLVER gesvd, of D^T when t > n), keeps the r <= 64 singular
                               triplets above 1e-15 s_0 (r rounded up to 8) and K2 contracts X_R' against the p r + t + r
                               columns [U_r (.) X_L'_f | d_j (.) y'_j | U_r] instead of t (p + 2); a K = r product with
                               W = S_r V_r^T restores the per-trait terms.  Error vs the exact weights ~ 1e-13 relative.

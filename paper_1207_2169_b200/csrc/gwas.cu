@@ -308,12 +308,14 @@ gwas_status solver_lwork(const gwas_options* o, int64_t n, int64_t kpad, int64_t
 // Device workspace (doubles) of cusolverDnDgesvd on the n x t trait-weight matrix D (low-rank mode), 0 if unused.
 gwas_status lr_lwork(const gwas_options* o, const Dims& d, int64_t* lwork) {
   *lwork = 0;
-  if (!d.lr || d.t > d.n) return GWAS_OK;
+  if (!d.lr) return GWAS_OK;
   CKC(cudaSetDevice(o->device));
   cusolverDnHandle_t h;
   CKS(cusolverDnCreate(&h));
   int lw = 0;
-  cusolverStatus_t st = cusolverDnDgesvd_bufferSize(h, (int)d.n, (int)d.t, &lw);
+  // gesvd needs m >= n: D (n x t) itself, or D^T when t > n
+  cusolverStatus_t st = d.t <= d.n ? cusolverDnDgesvd_bufferSize(h, (int)d.n, (int)d.t, &lw)
+                                   : cusolverDnDgesvd_bufferSize(h, (int)d.t, (int)d.n, &lw);
   cusolverDnDestroy(h);
   if (st != CUSOLVER_STATUS_SUCCESS) return fail(GWAS_E_CUDA, "cusolverDnDgesvd_bufferSize status %d", (int)st);
   *lwork = lw;
@@ -1016,22 +1018,34 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     c->h.lr_r = 0;
     c->h.lr_nsq = d.nsq;
     c->h.lr_nlin = d.nlin;
-    if (d.lr && t >= 16 && t <= n) {
+    if (d.lr && t >= 16) {
       double* A = reinterpret_cast<double*>(w + sl.lr_a);
       double* U = reinterpret_cast<double*>(w + sl.lr_u);
       double* VT = reinterpret_cast<double*>(w + sl.lr_vt);
       double* S = reinterpret_cast<double*>(w + sl.lr_s);
-      CKC(cudaMemcpy2DAsync(A, sizeof(double) * d.kpad, c->B2() + d.nsq * d.kpad, sizeof(double) * d.kpad,
-                            sizeof(double) * n, t, cudaMemcpyDeviceToDevice, cs));
+      const bool tall = t <= n;  // gesvd needs m >= n: factor D (n x t), else D^T (t x n)
+      const int64_t ns = std::min<int64_t>(n, t);
+      if (tall) {
+        CKC(cudaMemcpy2DAsync(A, sizeof(double) * d.kpad, c->B2() + d.nsq * d.kpad, sizeof(double) * d.kpad,
+                              sizeof(double) * n, t, cudaMemcpyDeviceToDevice, cs));
+      } else {
+        gw::rows_to_colmajor<<<(unsigned)((t * n + 255) / 256), 256, 0, cs>>>(c->B2() + d.nsq * d.kpad, d.kpad,
+                                                                               (int)t, (int)n, A, t);
+        CKC(cudaGetLastError());
+      }
       cusolverDnHandle_t hv;
       CKS(cusolverDnCreate(&hv));
       cusolverStatus_t sv = cusolverDnSetStream(hv, cs);
-      if (sv == CUSOLVER_STATUS_SUCCESS)
-        sv = cusolverDnDgesvd(hv, 'S', 'S', (int)n, (int)t, A, (int)d.kpad, S, U, (int)d.kpad, VT, (int)t,
-                              reinterpret_cast<double*>(w + sl.lr_work), (int)std::max<int64_t>(lrw, 1), nullptr,
-                              dinfo);
-      std::vector<double> hs(t);
-      CKC(cudaMemcpyAsync(hs.data(), S, sizeof(double) * t, cudaMemcpyDeviceToHost, cs));
+      if (sv == CUSOLVER_STATUS_SUCCESS) {
+        double* lw_ptr = reinterpret_cast<double*>(w + sl.lr_work);
+        const int lw_n = (int)std::max<int64_t>(lrw, 1);
+        sv = tall ? cusolverDnDgesvd(hv, 'S', 'S', (int)n, (int)t, A, (int)d.kpad, S, U, (int)d.kpad, VT, (int)t,
+                                     lw_ptr, lw_n, nullptr, dinfo)
+                  : cusolverDnDgesvd(hv, 'S', 'S', (int)t, (int)n, A, (int)t, S, U, (int)t, VT, (int)n, lw_ptr,
+                                     lw_n, nullptr, dinfo);
+      }
+      std::vector<double> hs(ns);
+      CKC(cudaMemcpyAsync(hs.data(), S, sizeof(double) * ns, cudaMemcpyDeviceToHost, cs));
       int sinfo = 0;
       CKC(cudaMemcpyAsync(&sinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, cs));
       CKC(cudaStreamSynchronize(cs));
@@ -1039,24 +1053,28 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
       if (sv != CUSOLVER_STATUS_SUCCESS || sinfo != 0)
         return fail(GWAS_E_EIG, "gesvd of the trait weights: status %d info %d", (int)sv, sinfo);
       int64_t r = 0;
-      while (r < t && hs[r] > kLrTol * hs[0]) ++r;
+      while (r < ns && hs[r] > kLrTol * hs[0]) ++r;
       r = std::max<int64_t>(8, round_up(r, 8));
       if (r <= kLrMax && 2 * r < t) {
         const int64_t nsq_lr = round_up(p * r + t, 32);
         double* nb2 = reinterpret_cast<double*>(w + sl.lr_b2);
         dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)(nsq_lr + r));
-        gw::build_lowrank_b2<<<grid, 256, 0, cs>>>(U, d.kpad, xlp, c->B2(), (int)n, (int)p, (int)t, (int)d.kpad,
-                                                   (int)r, (int)nsq_lr, nb2);
+        // D = U S V^T: tall -> U (n x t, ld kpad), V^T (t x t, ld t); wide -> D^T = U' S V'^T, i.e. U = V'
+        // (rows of VT, ld n) and V = U' (t x n, ld t)
+        const long long su_k = tall ? 1 : n, su_r = tall ? d.kpad : 1;
+        const long long sv_j = tall ? t : 1, sv_r = tall ? 1 : t;
+        gw::build_lowrank_b2<<<grid, 256, 0, cs>>>(tall ? U : VT, su_k, su_r, xlp, c->B2(), (int)n, (int)p, (int)t,
+                                                   (int)d.kpad, (int)r, (int)nsq_lr, nb2);
         CKC(cudaGetLastError());
         CKC(cudaMemcpyAsync(c->B2(), nb2, sizeof(double) * (nsq_lr + r) * d.kpad, cudaMemcpyDeviceToDevice, cs));
         gw::build_lowrank_wt<<<(unsigned)((t * r + 255) / 256), 256, 0, cs>>>(
-            S, VT, (int)t, (int)r, reinterpret_cast<double*>(c->state + c->h.off_wt));
+            S, tall ? VT : U, sv_j, sv_r, (int)t, (int)r, reinterpret_cast<double*>(c->state + c->h.off_wt));
         CKC(cudaGetLastError());
         c->h.lr_r = (int32_t)r;
         c->h.lr_nsq = nsq_lr;
         c->h.lr_nlin = p * r + t;
         c->h.lr_s0 = hs[0];
-        c->h.lr_sr = r < t ? hs[r] : 0.0;
+        c->h.lr_sr = r < ns ? hs[r] : 0.0;
       }
       CKC(cudaMemcpyAsync(c->state, &c->h, sizeof(StateHeader), cudaMemcpyHostToDevice, cs));
       CKC(cudaStreamSynchronize(cs));

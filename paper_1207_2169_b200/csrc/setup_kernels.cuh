@@ -122,9 +122,10 @@ namespace gw {
 //   row f r + rr (f < p) :  U[:, rr] * X_L'[:, f]          row p r + j :  B2_old row p t + j  (= d_j * y'_j)
 //   rows p r + t .. nsq_lr - 1 : 0                          row nsq_lr + rr :  U[:, rr]        (used with A∘A)
 // written to `out` (not in place: the y rows move up).
-__global__ void build_lowrank_b2(const double* __restrict__ U, long long ldu, const double* __restrict__ XLp,
-                                 const double* __restrict__ B2, int n, int p, int t, int kpad, int r, int nsq_lr,
-                                 double* __restrict__ out) {
+// U(k, rr) = U[k su_k + rr su_r] (column-major U of D, or the transposed VT of D^T when t > n).
+__global__ void build_lowrank_b2(const double* __restrict__ U, long long su_k, long long su_r,
+                                 const double* __restrict__ XLp, const double* __restrict__ B2, int n, int p, int t,
+                                 int kpad, int r, int nsq_lr, double* __restrict__ out) {
   const int row = blockIdx.y;
   double* o = out + (long long)row * kpad;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x) {
@@ -132,24 +133,33 @@ __global__ void build_lowrank_b2(const double* __restrict__ U, long long ldu, co
     if (k < n) {
       if (row < p * r) {
         const int f = row / r, rr = row - f * r;
-        v = U[(long long)rr * ldu + k] * XLp[(long long)f * kpad + k];
+        v = U[(long long)k * su_k + (long long)rr * su_r] * XLp[(long long)f * kpad + k];
       } else if (row < p * r + t) {
         v = B2[(long long)(p * t + (row - p * r)) * kpad + k];
       } else if (row >= nsq_lr) {
-        v = U[(long long)(row - nsq_lr) * ldu + k];
+        v = U[(long long)k * su_k + (long long)(row - nsq_lr) * su_r];
       }
     }
     o[k] = v;
   }
 }
 
-// W^T (t x r, row j = the trait's r mixing weights): Wt[j][rr] = S[rr] VT[rr][j]  (VT column-major, ld t).
-__global__ void build_lowrank_wt(const double* __restrict__ S, const double* __restrict__ VT, int t, int r,
-                                 double* __restrict__ Wt) {
+// W^T (t x r, row j = the trait's r mixing weights): Wt[j][rr] = S[rr] V(j, rr), V(j, rr) = V[j sv_j + rr sv_r].
+__global__ void build_lowrank_wt(const double* __restrict__ S, const double* __restrict__ V, long long sv_j,
+                                 long long sv_r, int t, int r, double* __restrict__ Wt) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= t * r) return;
   const int j = idx / r, rr = idx - j * r;
-  Wt[idx] = S[rr] * VT[(long long)j * t + rr];
+  Wt[idx] = S[rr] * V[(long long)j * sv_j + (long long)rr * sv_r];
+}
+
+// dst (rows x cols, column-major, ld ldd) = the rows x cols matrix stored row-major in src (row stride lds).
+__global__ void rows_to_colmajor(const double* __restrict__ src, long long lds, int rows, int cols,
+                                 double* __restrict__ dst, long long ldd) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * cols) return;
+  const int r = (int)(idx % rows), c = (int)(idx / rows);
+  dst[(long long)c * ldd + r] = src[(long long)r * lds + c];
 }
 
 }  // namespace gw

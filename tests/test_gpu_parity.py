@@ -567,3 +567,24 @@ def test_sigma2_scaling_on_gpu():
     np.testing.assert_array_equal(s1, s2)
     np.testing.assert_allclose(b2, b1, rtol=1e-12, atol=0)
     np.testing.assert_allclose(v2, 4.0 * v1, rtol=1e-12)
+
+
+@pytest.mark.parametrize("i8", [0, 7])
+def test_lowrank_more_traits_than_individuals(i8):
+    """t > n (the paper's omics scenario C has t up to 1e5 at n = 1e3): D^T is factored instead of D."""
+    gw = _gw()
+    cfg = datagen.custom_config(n=120, p=3, m=400, t=300, index=473)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=256, int8_slices=i8, trait_rank=-1)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    r, s0, sr = eng.trait_rank()
+    assert 8 <= r <= 40 and sr <= 1e-15 * s0, (r, s0, sr)
+    b, v, s = eng.run(torch.from_numpy(XR).cuda())
+    torch.cuda.synchronize()
+    res = (b.cpu().numpy(), v.cpu().numpy(), s.cpu().numpy())
+    eng.close()
+    eb, ev = compare(*res, ref)
+    print(f"low-rank t > n: r={r} max|db|/SE={eb:.2e} Var rel={ev:.2e}")
+    assert eb <= TOL_B and ev <= TOL_VAR
