@@ -585,18 +585,18 @@ __global__ void digitize_rows(const double* __restrict__ X, long long ldx, int r
 // CLAK-Chol setup (Alg. 3 line 1): M = sigma2 (h2 Phi + (1 - h2) I) in place over a copy of Phi
 // (column-major, ld kpad), both triangles from one expression per entry.
 __global__ void assemble_m(double* __restrict__ A, int n, int kpad, double sigma2, double h2) {
-  const int c = blockIdx.y;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const double phi = A[(long long)c * kpad + r];
-    A[(long long)c * kpad + r] = sigma2 * (h2 * phi + (r == c ? 1.0 - h2 : 0.0));
-  }
+  for (int c = blockIdx.y; c < n; c += gridDim.y)  // grid-stride in y: n may exceed the 65535 grid limit
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+      const double phi = A[(long long)c * kpad + r];
+      A[(long long)c * kpad + r] = sigma2 * (h2 * phi + (r == c ? 1.0 - h2 : 0.0));
+    }
 }
 
 // Zero the strict upper triangle (and the padding) of a column-major kpad x kpad matrix (dtrtri leaves M there).
 __global__ void zero_upper(double* __restrict__ A, int n, int kpad) {
-  const int c = blockIdx.y;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < kpad; r += gridDim.x * blockDim.x)
-    if (r < c || r >= n || c >= n) A[(long long)c * kpad + r] = 0.0;
+  for (int c = blockIdx.y; c < kpad; c += gridDim.y)
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < kpad; r += gridDim.x * blockDim.x)
+      if (r < c || r >= n || c >= n) A[(long long)c * kpad + r] = 0.0;
 }
 
 // Out-of-place transpose of a kpad x kpad fp64 matrix (tiled through shared memory).

@@ -260,7 +260,7 @@ gwas_status check_sizes(int64_t n, int64_t p, int64_t t, const gwas_options* o) 
   if (o->output_mode != GWAS_OUT_SNP && o->output_mode != GWAS_OUT_FULL) return fail(GWAS_E_ARG, "bad output_mode");
   if (o->var_convention != GWAS_VAR_TEXTBOOK && o->var_convention != GWAS_VAR_LITERAL)
     return fail(GWAS_E_ARG, "bad var_convention");
-  if (o->block_cols < 0 || o->block_cols > (1ll << 22)) return fail(GWAS_E_ARG, "bad block_cols");
+  if (o->block_cols < 0 || o->block_cols > (1ll << 20)) return fail(GWAS_E_ARG, "bad block_cols (0 or <= 2^20)");
   if (!(o->eps_spd >= 0) || !(o->eps_collinear >= 0)) return fail(GWAS_E_ARG, "bad eps");
   const int64_t t_p2 = t * (p + 2) + 8;
   if (t_p2 > (1ll << 31) - 1) return fail(GWAS_E_ARG, "t too large");
@@ -948,7 +948,8 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
       const int64_t slw = lwork - d.kpad * d.kpad;
       CKC(cudaMemcpy2DAsync(Mw, sizeof(double) * d.kpad, c->Z(), sizeof(double) * d.kpad, sizeof(double) * d.kpad,
                             d.kpad, cudaMemcpyDeviceToDevice, cs));
-      gw::assemble_m<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n), 256, 0, cs>>>(
+      gw::assemble_m<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535)),
+                        256, 0, cs>>>(
           Mw, (int)n, (int)d.kpad, ss[0], hh[0]);
       CKC(cudaGetLastError());
       if (ss2 == CUSOLVER_STATUS_SUCCESS)
@@ -964,7 +965,8 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
       if (ss2 == CUSOLVER_STATUS_SUCCESS)
         ss2 = cusolverDnXtrtri(hs, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, Mw, d.kpad, sw,
                                (size_t)slw * sizeof(double), host_ws_buf.data(), host_ws, dinfo);
-      gw::zero_upper<<<dim3((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)d.kpad), 256, 0, cs>>>(
+      gw::zero_upper<<<dim3((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64),
+                            (unsigned)std::min<int64_t>(d.kpad, 65535)), 256, 0, cs>>>(
           Mw, (int)n, (int)d.kpad);
       CKC(cudaGetLastError());
       gw::transpose_sq<<<dim3((unsigned)((d.kpad + 31) / 32), (unsigned)((d.kpad + 31) / 32)), dim3(32, 8), 0, cs>>>(
@@ -1001,7 +1003,7 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     }
     // Alg. 4 lines 6, 8, 9: D_j and the D_j-scaled operand B2 = [B_op | D]
     {
-      dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)d.n2);
+      dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)std::min<int64_t>(d.n2, 65535));
       gw::build_b2<<<grid, 256, 0, cs>>>(xlp, yp, c->W(), dh2, ds2, (int)n, (int)p, (int)t, (int)d.kpad, (int)d.nsq,
                                          (int)d.n2, o->eps_spd, c->B2(), derr);
       CKC(cudaGetLastError());
@@ -1058,7 +1060,7 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
       if (r <= kLrMax && 2 * r < t) {
         const int64_t nsq_lr = round_up(p * r + t, 32);
         double* nb2 = reinterpret_cast<double*>(w + sl.lr_b2);
-        dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)(nsq_lr + r));
+        dim3 grid((unsigned)std::min<int64_t>((d.kpad + 255) / 256, 64), (unsigned)std::min<int64_t>(nsq_lr + r, 65535));
         // D = U S V^T: tall -> U (n x t, ld kpad), V^T (t x t, ld t); wide -> D^T = U' S V'^T, i.e. U = V'
         // (rows of VT, ld n) and V = U' (t x n, ld t)
         const long long su_k = tall ? 1 : n, su_r = tall ? d.kpad : 1;

@@ -61,22 +61,36 @@ __global__ void __launch_bounds__(128) schur_solve(SchurArgs s) {
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
   const int i0 = (blockIdx.y * (blockDim.x / s.tj) + ii) * s.ich;
   const int i1 = min(s.cols, i0 + s.ich);
-  for (int i = i0; i < i1; ++i) {
+  // the P + 2 inputs of the next pair are loaded while the current one is solved (memory-level parallelism:
+  // the kernel is HBM-bound, each thread walks its SNP chunk sequentially)
+  double nxt[P + 2];
+  auto load = [&](int i, double (&x)[P + 2]) {
     const double* row = s.C + (long long)i * s.ldc;
+#pragma unroll
+    for (int f = 0; f < P; ++f) x[f] = __ldg(row + f * t + j);
+    x[P] = __ldg(s.Cy + (long long)i * s.ldcy + j);
+    x[P + 1] = __ldg(row + s.nsq + j);
+  };
+  if (i0 < i1) load(i0, nxt);
+  for (int i = i0; i < i1; ++i) {
+    double cur[P + 2];
+#pragma unroll
+    for (int f = 0; f < P + 2; ++f) cur[f] = nxt[f];
+    if (i + 1 < i1) load(i + 1, nxt);
     const long long idx = (long long)i * t + j;
     double u[P];
     double uv = 0.0, uu = 0.0;
 #pragma unroll
     for (int f = 0; f < P; ++f) {
-      double acc = __ldg(row + f * t + j);
+      double acc = cur[f];
 #pragma unroll
       for (int l = 0; l < f; ++l) acc -= L[f * (f + 1) / 2 + l] * u[l];
       u[f] = acc * Linv_d[f];
       uu += u[f] * u[f];
       uv += u[f] * v[f];
     }
-    const double r = __ldg(s.Cy + (long long)i * s.ldcy + j);
-    const double c = __ldg(row + s.nsq + j);
+    const double r = cur[P];
+    const double c = cur[P + 1];
     const double sigma = c - uu;
     int8_t st = 0;
     if (!(isfinite(sigma) && isfinite(c) && isfinite(r) && isfinite(uv))) st = 2;

@@ -15,8 +15,7 @@ namespace gw {
 __global__ void build_b2(const double* __restrict__ XLp, const double* __restrict__ Yp, const double* __restrict__ W,
                          const double* __restrict__ h2, const double* __restrict__ s2, int n, int p, int t, int kpad,
                          int nsq, int n2, double eps_spd, double* __restrict__ B2, unsigned long long* err) {
-  const int col = blockIdx.y;
-  if (col >= n2) return;
+  for (int col = blockIdx.y; col < n2; col += gridDim.y) {  // grid-stride in y: n2 = t (p + 2) may exceed 65535
   int j = -1, f = -1;
   if (col < t * (p + 1)) {
     f = col / t;
@@ -39,6 +38,7 @@ __global__ void build_b2(const double* __restrict__ XLp, const double* __restric
       else val = d * Yp[(long long)j * kpad + k];
     }
     out[k] = val;
+  }
   }
 }
 
@@ -107,10 +107,9 @@ __global__ void trait_factor(const double* __restrict__ STL, long long lds, int 
 // Column-major n x c (ld = ld_src) -> row-per-column layout with leading dimension kpad, zero padding.
 __global__ void pad_columns(const double* __restrict__ src, long long ld_src, int n, int c, int kpad,
                             double* __restrict__ dst) {
-  const int col = blockIdx.y;
-  if (col >= c) return;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x)
-    dst[(long long)col * kpad + k] = (k < n) ? src[(long long)col * ld_src + k] : 0.0;
+  for (int col = blockIdx.y; col < c; col += gridDim.y)
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x)
+      dst[(long long)col * kpad + k] = (k < n) ? src[(long long)col * ld_src + k] : 0.0;
 }
 
 }  // namespace gw
@@ -126,7 +125,7 @@ namespace gw {
 __global__ void build_lowrank_b2(const double* __restrict__ U, long long su_k, long long su_r,
                                  const double* __restrict__ XLp, const double* __restrict__ B2, int n, int p, int t,
                                  int kpad, int r, int nsq_lr, double* __restrict__ out) {
-  const int row = blockIdx.y;
+  for (int row = blockIdx.y; row < nsq_lr + r; row += gridDim.y) {
   double* o = out + (long long)row * kpad;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x) {
     double v = 0.0;
@@ -141,6 +140,7 @@ __global__ void build_lowrank_b2(const double* __restrict__ U, long long su_k, l
       }
     }
     o[k] = v;
+  }
   }
 }
 

@@ -588,3 +588,16 @@ def test_lowrank_more_traits_than_individuals(i8):
     eb, ev = compare(*res, ref)
     print(f"low-rank t > n: r={r} max|db|/SE={eb:.2e} Var rel={ev:.2e}")
     assert eb <= TOL_B and ev <= TOL_VAR
+
+
+@pytest.mark.parametrize("lr", [0, -1])
+def test_many_traits_beyond_grid_limit(lr):
+    """t (p + 2) > 65535 operand rows (grid-stride setup kernels), checked on a seeded subset of traits."""
+    cfg = datagen.custom_config(n=64, p=2, m=96, t=16500, index=474)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(cfg.n))
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), block_cols=64, trait_rank=lr)
+    traits = np.unique(np.concatenate([[0, cfg.t - 1], np.random.default_rng(0).choice(cfg.t, 30, replace=False)]))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2, traits=traits)
+    eb, ev = compare(b[:, traits], v[:, traits], s[:, traits], ref)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
