@@ -36,7 +36,9 @@
  *                           16 -> 6.8, 32 -> 9.8, 64 -> 17.5 GB; time 32.4-32.6 ms for all: DMMA-bound)
  *   GWAS_I8_TRACE=<file>    append %globaltimer phase stamps of the int8 kernel to <file> (allocates a 256 KB
  *                           device buffer and synchronises after every launch)
- *   GWAS_I8_DBG=1|2         int8 epilogue without TMEM loads / stores (timing experiments; results invalid) */
+ *   GWAS_I8_DBG=1|2         int8 epilogue without TMEM loads / stores (timing experiments; results invalid)
+ *   GWAS_LR_UNFUSED=1       low-rank mode: separate K = r recombination products + K3 instead of the fused kernel
+ *                           (even t only; results equal up to rounding) */
 #ifndef GWAS_H
 #define GWAS_H
 

@@ -19,6 +19,7 @@
 #include "gemm_dmma.cuh"
 #include "estimate_launch.cuh"
 #include "gemm_i8.cuh"
+#include "lowrank_k3.cuh"
 #include "schur.cuh"
 #include "setup_kernels.cuh"
 
@@ -490,6 +491,24 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
                                                                        kSplitLd, c_final, ldc_final);
     CKC(cudaGetLastError());
   }
+  return GWAS_OK;
+}
+
+// K3 fused with the low-rank recombination (lowrank_k3.cuh): grid of 32-trait x 64-SNP tiles.
+gwas_status launch_lowrank_schur(const gw::LowrankK3Args& a, int p, cudaStream_t st) {
+  if ((long long)a.k3.cols * a.k3.t == 0) return GWAS_OK;
+  const dim3 grid((unsigned)((a.k3.t + gw::LRK3_COLS - 1) / gw::LRK3_COLS),
+                  (unsigned)((a.k3.cols + gw::LRK3_ROWS - 1) / gw::LRK3_ROWS));
+  switch (p) {
+#define CASE_P(P) \
+  case P: gw::lowrank_schur<P><<<grid, gw::LRK3_THREADS, 0, st>>>(a); break;
+    CASE_P(1) CASE_P(2) CASE_P(3) CASE_P(4) CASE_P(5) CASE_P(6)
+    CASE_P(7) CASE_P(8) CASE_P(9) CASE_P(10) CASE_P(11) CASE_P(12)
+#undef CASE_P
+    default:
+      return fail(GWAS_E_ARG, "p = %d unsupported", p);
+  }
+  CKC(cudaGetLastError());
   return GWAS_OK;
 }
 
@@ -1237,6 +1256,9 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
   const bool u8 = c->opt.xr_dtype == GWAS_XR_U8;
   const bool chol = c->opt.algorithm == GWAS_ALG_CHOL;
   const int64_t lr_r = c->h.lr_r, lr_nsq = c->h.lr_nsq, lr_nlin = c->h.lr_nlin;
+  // low-rank: K3 fused with the K = r recombination (GWAS_LR_UNFUSED=1: separate products + K3, for comparison)
+  static const bool lr_unfused_env = getenv("GWAS_LR_UNFUSED") != nullptr;
+  const bool lr_fused = lr_r > 0 && (!lr_unfused_env || (d.t & 1));  // the separate products need even t (alignment)
   const int64_t w = d.p + 1;
   const int64_t per_pair = c->opt.output_mode == GWAS_OUT_FULL ? w : 1;
   cudaStream_t cs = c->cs, ps = c->ps;
@@ -1316,7 +1338,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       } else if (lr_r > 0) {  // low-rank trait weights: the products against U_r, then the recombination with W
         CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, g2, d.ldg2, cols, lr_nsq + lr_r, d.n, lr_nsq, cs2, 16,
                     splitbuf));
-        CKG(lowrank_recombine(c, g2, c2, cols, cs2));
+        if (!lr_fused) CKG(lowrank_recombine(c, g2, c2, cols, cs2));
       } else {
         static const int k2_group = getenv("GWAS_K2_GROUP") ? atoi(getenv("GWAS_K2_GROUP")) : 16;
         CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, k2_group,
@@ -1346,7 +1368,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       } else if (lr_r > 0) {  // low-rank: X_R'^2 against the r columns of U_r, then the recombination with W
         CKG(gemm_tn(false, xrp, d.kpad, c->B2() + lr_nsq * d.kpad, d.kpad, g2 + lr_nsq, d.ldg2, cols, lr_r, d.n,
                     lr_r, cs2, 16, splitbuf));
-        CKG(lowrank_recombine(c, g2, c2, cols, cs2));
+        if (!lr_fused) CKG(lowrank_recombine(c, g2, c2, cols, cs2));
       } else {
         // xrp holds X_R'^2 (squared in K1i's epilogue), so this is a plain product (nsq = N: no squaring)
         CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, d.t,
@@ -1384,7 +1406,18 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
       a.status = reinterpret_cast<int8_t*>(a.var + cols * d.t * per_pair);
     }
     CKG(c->tic(GWAS_K3, cs2, &dummy));
-    CKG(launch_schur(a, (int)d.p, cs2));
+    if (lr_fused) {  // the recombination products and K3 in one kernel (lowrank_k3.cuh)
+      gw::LowrankK3Args la;
+      la.G = g2;
+      la.ldg = d.ldg2;
+      la.r = (int)lr_r;
+      la.nsq_lr = (int)lr_nsq;
+      la.Wt = reinterpret_cast<const double*>(c->state + c->h.off_wt);
+      la.k3 = a;
+      CKG(launch_lowrank_schur(la, (int)d.p, cs2));
+    } else {
+      CKG(launch_schur(a, (int)d.p, cs2));
+    }
     CKG(c->toc(cs2));
     if (ovl) CKC(cudaEventRecord(c->ev_set_free[set], cs2));
     if (!out_dev) {  // stream this block's results to the caller's pinned host buffers, overlapped with compute

@@ -601,3 +601,38 @@ def test_many_traits_beyond_grid_limit(lr):
     ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2, traits=traits)
     eb, ev = compare(b[:, traits], v[:, traits], s[:, traits], ref)
     assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+def test_lowrank_fused_k3_matches_unfused():
+    """The fused recombination + Schur kernel against the separate K = r products + K3 (GWAS_LR_UNFUSED=1), and
+    both against the oracle (full output mode, t not a multiple of the 32-trait tile, ragged SNP block)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np, torch, datagen; sys.path.insert(0, 'tests');"
+            "import paper_1207_2169_b200 as gw;"
+            "cfg = datagen.custom_config(n=200, p=4, m=333, t=77, index=475); ds = datagen.dataset(cfg);"
+            "X = torch.from_numpy(datagen.xr_dosages(cfg, ld=208)).cuda();"
+            "e = gw.Gwas(cfg.n, cfg.p, cfg.t, trait_rank=-1, block_cols=150, output_mode='full');"
+            "e.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2); b, v, s = e.run(X); torch.cuda.synchronize();"
+            "np.savez(sys.argv[1], b=b.cpu().numpy(), v=v.cpu().numpy(), s=s.cpu().numpy(), r=e.trait_rank()[0])")
+    import tempfile
+    outs = []
+    with tempfile.TemporaryDirectory() as d:
+        for i, unfused in enumerate((False, True)):
+            f = os.path.join(d, f"r{i}.npz")
+            env = dict(os.environ)
+            if unfused:
+                env["GWAS_LR_UNFUSED"] = "1"
+            subprocess.run([sys.executable, "-c", code, f], check=True, env=env,
+                           cwd=os.path.dirname(os.path.dirname(__file__)))
+            outs.append(np.load(f))
+    assert outs[0]["r"] > 0
+    cfg = datagen.custom_config(n=200, p=4, m=333, t=77, index=475)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=208)
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    for o in outs:
+        eb, ev = compare(o["b"], o["v"], o["s"], ref, full=True)
+        assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+    np.testing.assert_array_equal(outs[0]["s"], outs[1]["s"])
