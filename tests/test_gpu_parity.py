@@ -605,13 +605,14 @@ def test_many_traits_beyond_grid_limit(lr):
 
 def test_lowrank_fused_k3_matches_unfused():
     """The fused recombination + Schur kernel against the separate K = r products + K3 (GWAS_LR_UNFUSED=1), and
-    both against the oracle (full output mode, t not a multiple of the 32-trait tile, ragged SNP block)."""
+    both against the oracle (full output mode, t = 78 not a multiple of the 32-trait tile, ragged SNP block; the
+    separate products need even t)."""
     import os
     import subprocess
     import sys
     code = ("import sys, numpy as np, torch, datagen; sys.path.insert(0, 'tests');"
             "import paper_1207_2169_b200 as gw;"
-            "cfg = datagen.custom_config(n=200, p=4, m=333, t=77, index=475); ds = datagen.dataset(cfg);"
+            "cfg = datagen.custom_config(n=200, p=4, m=333, t=78, index=475); ds = datagen.dataset(cfg);"
             "X = torch.from_numpy(datagen.xr_dosages(cfg, ld=208)).cuda();"
             "e = gw.Gwas(cfg.n, cfg.p, cfg.t, trait_rank=-1, block_cols=150, output_mode='full');"
             "e.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2); b, v, s = e.run(X); torch.cuda.synchronize();"
@@ -628,7 +629,7 @@ def test_lowrank_fused_k3_matches_unfused():
                            cwd=os.path.dirname(os.path.dirname(__file__)))
             outs.append(np.load(f))
     assert outs[0]["r"] > 0
-    cfg = datagen.custom_config(n=200, p=4, m=333, t=77, index=475)
+    cfg = datagen.custom_config(n=200, p=4, m=333, t=78, index=475)
     ds = datagen.dataset(cfg)
     XR = datagen.xr_dosages(cfg, ld=208)
     ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :cfg.n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
