@@ -28,6 +28,7 @@ namespace {
 constexpr uint64_t kMagic = 0x4b414c4353415747ull;  // "GWASCLAK"
 constexpr int64_t kVersion = 1;
 constexpr int kPMax = 12;
+constexpr int kWideSplitN = 1024;   // widest fp64 product split 2-way along K (int8 K2b; gemm_tn wide_split)
 constexpr int kLrMax = 64;          // largest trait-weight rank kept (low-rank mode)
 constexpr double kLrTol = 1e-15;    // singular values of D below kLrTol * s_0 are dropped (reading L1)
 
@@ -170,7 +171,7 @@ StateHeader make_header(const Dims& d, const gwas_options* o) {
 }
 
 struct RunLayout {
-  size_t stage[2], xrp[2], c2[2], split[2], outb[2], fp[2], g2[2], total;
+  size_t stage[2], xrp[2], c2[2], split[2], outb[2], fp[2], g2[2], wsplit[2], total;
   size_t out_bytes;  // per staging set: b, var (8 * per_pair each) + status (1) per pair of a block
 };
 // overlap mode double-buffers the rotated block and the K2 output so block b+1's K1 can run beside block b's K2/K3
@@ -194,6 +195,11 @@ RunLayout run_layout(const Dims& d, bool overlap) {
   r.out_bytes = (size_t)d.kb * d.t * (16 * d.per_pair + 1);
   r.outb[0] = take(r.out_bytes);
   r.outb[1] = take(r.out_bytes);
+  r.wsplit[0] = r.wsplit[1] = 0;
+  if (d.i8 && d.t > 64 && d.t <= kWideSplitN && d.n >= 4096) {  // 2-way K split of K2b (gemm_tn wide_split)
+    r.wsplit[0] = take(sizeof(double) * 2 * round_up(d.t, 2) * d.kb);
+    r.wsplit[1] = overlap ? take(sizeof(double) * 2 * round_up(d.t, 2) * d.kb) : r.wsplit[0];
+  }
   r.g2[0] = r.g2[1] = 0;
   if (d.lr) {  // low-rank K2 output [U_r-projected fields | y | pad | squared]
     r.g2[0] = take(sizeof(double) * d.ldg2 * d.kb);
@@ -394,7 +400,7 @@ constexpr int kSplitMax = 8, kSplitLd = 64;
 gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                     int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st, int group_m = 16,
                     double* split_scratch = nullptr, bool tri = false, const gw::GemmShape* fuse = nullptr,
-                    int* tiles_n_out = nullptr) {
+                    int* tiles_n_out = nullptr, double* wide_split_scratch = nullptr) {
   if (M <= 0 || N <= 0) return GWAS_OK;
   if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
   if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
@@ -415,6 +421,11 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
     const double cost128 = (double)((tiles128 + 147) / 148), cost64 = (double)((tiles64 + 147) / 148) * 0.5 / 0.93;
     bn = cost64 < cost128 ? 64 : 128;
   }
+  // Medium-width fp64 products with a long K (int8 mode's K2b at t <= 1024, n >= 4096): 128-wide tiles split 2-way
+  // along K (fixed halves, chosen from N and K only: bitwise invariant to the block size) instead of 64-wide tiles
+  const int kt_all0 = (int)((K + gw::GEMM_BK - 1) / gw::GEMM_BK);
+  const bool wide_split = wide_split_scratch && !fuse && !a_u8 && N > 64 && N <= kWideSplitN && kt_all0 >= 256;
+  if (wide_split) bn = 128;
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, a_u8, K, M, lda, kBM));
   CKG(make_map(&mb, B, false, K, N, ldb, bn));
@@ -451,12 +462,20 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   }
   double* c_final = C;
   int64_t ldc_final = ldc;
+  int64_t split_ld = kSplitLd;
   if (split_scratch && !fuse && N <= kSplitLd && kt_all >= 16) {
     s.kt_per_split = std::max(8, (kt_all + kSplitMax - 1) / kSplitMax);
     s.ksplit = (kt_all + s.kt_per_split - 1) / s.kt_per_split;
     s.C = split_scratch;
     s.ldc = kSplitLd;
     s.split_stride = (long long)M * kSplitLd;
+  } else if (wide_split) {
+    split_ld = round_up(N, 2);
+    s.kt_per_split = (kt_all + 1) / 2;
+    s.ksplit = 2;
+    s.C = wide_split_scratch;
+    s.ldc = split_ld;
+    s.split_stride = (long long)M * split_ld;
   }
   const bool sq = nsq < N;
   if (sq && (nsq % 32)) return fail(GWAS_E_ARG, "nsq must be a multiple of 32");
@@ -488,7 +507,7 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   if (s.ksplit > 1) {
     const long long total = M * N;
     gw::splitk_reduce<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s.C, s.split_stride, s.ksplit, (int)M, (int)N,
-                                                                       kSplitLd, c_final, ldc_final);
+                                                                       split_ld, c_final, ldc_final);
     CKC(cudaGetLastError());
   }
   return GWAS_OK;
@@ -1371,8 +1390,9 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
         if (!lr_fused) CKG(lowrank_recombine(c, g2, c2, cols, cs2));
       } else {
         // xrp holds X_R'^2 (squared in K1i's epilogue), so this is a plain product (nsq = N: no squaring)
+        double* wsb = c->rl.wsplit[set] ? reinterpret_cast<double*>(c->work + c->rl.wsplit[set]) : nullptr;
         CKG(gemm_tn(false, xrp, d.kpad, c->B2() + d.nsq * d.kpad, d.kpad, c2 + d.nsq, d.ldc2, cols, d.t, d.n, d.t,
-                    cs2, 16, splitbuf));
+                    cs2, 16, splitbuf, false, nullptr, nullptr, wsb));
       }
       CKG(c->toc(cs2));
     }
