@@ -6,8 +6,8 @@
 // |b_c| 2^-e_c <= 127/128 and split into S signed 8-bit digits (balanced, round-to-nearest):
 //       b_c 2^-e_c = sum_{s<S} d_s 2^{-7(s+1)} + r,   |d_0| <= 127, |d_{s>0}| <= 64, |r| <= 2^{-7S-1}
 // Every digit product sum_r g[r,i] d_s[r,c] is an exact int32 on the tensor core (|.| <= 255*127*n < 2^31 for
-// n <= 66 000), and the fp64 epilogue recombines the S int32 accumulators (Horner in 2^-7, one rounding per
-// digit) and applies 2^e_c.  With S = 8 the representation error is <= 2^-57 of the column maximum.
+// n <= 66 000), and the epilogue recombines the S int32 accumulators exactly in two int64 halves, rounds once to
+// fp64 and applies 2^e_c.  The representation error is <= 2^-57 (S = 8) or 2^-50 (S = 7) of the column maximum.
 //
 // Used for B = Z (Alg. 4 line 3: X_R' = Z^T X_R, needed for the W_R^T W_R term) and for the re-associated
 // linear terms of lines 13-15: W_R^T W_L = X_R^T (Z D_j X_L') and W_R^T Y_j = X_R^T (Z D_j y'_j),
@@ -15,11 +15,11 @@
 // output tiles [0, na_tiles) write C_a (X_R'^T), the rest write C_b (the linear block of the K2 output).
 //
 // Kernel: one 128 x 64 output tile per CTA.  B rows of a tile are stacked digit-major (row s*64 + j = digit s
-// of output column j), so the S*64 = 512 int32 accumulators of the tile fill TMEM exactly (512 columns x 128
-// lanes).  Warp 0: TMA producer (A box 64 B x 128 rows, B boxes 64 B x 256 rows, 64-byte swizzle) into a
-// STAGES ring; warp 1: TMEM allocation + single-thread tcgen05.mma issue (M = 128, N = 256, K = 32 per
-// instruction, two instructions per K step), tcgen05.commit -> mbarriers; warps 4-7: epilogue
-// (tcgen05.ld 32x32b, Horner recombination, fp64 stores).
+// of output column j), so the S*64 (512 or 448) int32 accumulators of the tile fit TMEM's 512 columns x 128
+// lanes.  Warp 0: TMA producer (A box 64 B x 128 rows, B boxes of the S*64-row digit slab, 64-byte swizzle,
+// multicast across a 2-CTA cluster) into a STAGES ring; warp 1: TMEM allocation + single-thread tcgen05.mma issue
+// (M = 128, N = 256 and N = (S-4)*64, K = 32 per instruction), tcgen05.commit -> mbarriers; warps 4-7: epilogue
+// (tcgen05.ld 32x32b, exact int64 recombination, fp64 stores or the fused squared-term partials).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
