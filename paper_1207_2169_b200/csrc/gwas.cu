@@ -26,7 +26,7 @@
 namespace {
 
 constexpr uint64_t kMagic = 0x4b414c4353415747ull;  // "GWASCLAK"
-constexpr int64_t kVersion = 1;
+constexpr int64_t kVersion = 2;  // state layout: 2 adds the low-rank weights and 7-digit int8 fields
 constexpr int kPMax = 12;
 constexpr int kWideSplitN = 1024;   // widest fp64 product split 2-way along K (int8 K2b; gemm_tn wide_split)
 constexpr int kLrMax = 64;          // largest trait-weight rank kept (low-rank mode)
@@ -862,7 +862,9 @@ void gwas_default_options(gwas_options* o) {
 }
 
 const char* gwas_last_error(void) { return g_err.c_str(); }
-const char* gwas_version(void) { return "gwas-clak-eig-b200 1 (sm_100a, FP64 DMMA)"; }
+const char* gwas_version(void) {
+  return "gwas-clak-eig-b200 2 (sm_100a: FP64 DMMA, int8-sliced tcgen05, low-rank trait weights, ML/REML estimation)";
+}
 
 size_t gwas_state_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   if (check_sizes(n, p, t, o) != GWAS_OK) return 0;
