@@ -204,10 +204,17 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    # GWAS_BENCH_BACKEND=gloo (testing only): exercise the multi-rank path (broadcast + attach, max over ranks) with
+    # all ranks on the visible GPU(s); NCCL needs one GPU per rank.  Numbers from such a run are not bench values.
+    backend = os.environ.get("GWAS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_1207_2169_b200 as gw
 
     cfg = datagen.CONFIGS[args.config]

@@ -34,3 +34,22 @@ def test_bench_json_line_config0():
         assert k in d["clocks"], k
     assert d["parity"]["pass"] and d["modes"]["int8_sliced"]["parity"]["pass"]
     assert "estimate" in d["modes"]
+
+
+def test_bench_two_ranks_gloo_on_one_gpu():
+    """The multi-rank path of bench.py (state broadcast from rank 0, gwas_attach on rank 1, max over ranks, the
+    rank-0 parity check) with two processes sharing the visible GPU over gloo (GWAS_BENCH_BACKEND; testing only,
+    NCCL needs one GPU per rank).  The numbers of such a run are not measurements."""
+    pytest.importorskip("torch")
+    env = dict(os.environ, GWAS_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2",
+                          "--config", "0", "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-est-alt"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "snp-shard x2"
+    assert d["setup"]["broadcast_bytes"] > 0 and d["parity"]["pass"]
+    assert d["modes"]["int8_sliced"]["parity"]["pass"]
