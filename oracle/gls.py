@@ -25,7 +25,9 @@ is the definition, evaluated by the paper's own per-problem procedure, CLAK-Chol
 
 Steps 1-4 depend on (i, j) only through j and through the column g_i of X: `gls_sequence` therefore runs
 steps 1-2 once per trait and step 3 once per needed column -- the same numbers the per-pair loop would
-produce, column by column (test_oracle.py checks it against `gls_single` per pair).  Nothing is blocked,
+produce, column by column.  Both entry points run the same primitives on the same shapes (the substitution
+always has the X_L columns plus >= 1 SNP column as right-hand sides; lines 5-7 on a stack), so the trait-cached
+sequence is bitwise equal to the literal per-pair Alg. 1 (test_oracle.py asserts it).  Nothing is blocked,
 fused or reordered beyond that; no eigendecomposition appears anywhere in the oracle.
 
 Collinearity (reading A6): in step 7 the last pivot R_ww^2 of S equals the Schur complement of the SNP
@@ -101,6 +103,16 @@ def small_spd_solve(R: np.ndarray, rhs: np.ndarray) -> np.ndarray:
     return x[..., 0] if vec else x
 
 
+def normal_equations(Xw: np.ndarray, yw: np.ndarray):
+    """Alg. 1 lines 5-6 on a stack of whitened designs Xw (k, n, w) and one whitened y (n,):
+    S = X^T X (k, w, w), r = X^T y (k, w).  Each entry is the same dot product whatever k is."""
+    Xw = np.ascontiguousarray(Xw)   # one memory layout, so one summation order, whatever the caller passed
+    yw = np.ascontiguousarray(yw)
+    S = np.einsum("kna,knb->kab", Xw, Xw)
+    r = np.einsum("kna,n->ka", Xw, yw)
+    return S, r
+
+
 def _finish(S, r, sigma2, eps_collinear, var_convention):
     """Steps 7 (+Var) on a stack of normal equations S (..., w, w), r (..., w).
     Returns b (..., w), Var (..., w, w), status (...)."""
@@ -134,10 +146,9 @@ def gls_single(Phi, X, y, sigma2, h2, var_convention=0, eps_collinear=1e-10):
     L = cholesky_lower(M)                              # line 2
     Xw = forward_substitute(L, X)                      # line 3
     yw = forward_substitute(L, y)                      # line 4
-    S = Xw.T @ Xw                                      # line 5
-    r = Xw.T @ yw                                      # line 6
-    b, Var, st = _finish(S, r, sigma2, eps_collinear, var_convention)  # line 7
-    return b, Var, int(st)
+    S, r = normal_equations(Xw[None], yw)              # lines 5-6
+    b, Var, st = _finish(S, r, np.array([sigma2], dtype=np.float64), eps_collinear, var_convention)  # line 7
+    return b[0], Var[0], int(st[0])
 
 
 def gls_sequence(Phi, XL, XR, Y, h2, sigma2, snps=None, traits=None, var_convention=0,
@@ -163,17 +174,17 @@ def gls_sequence(Phi, XL, XR, Y, h2, sigma2, snps=None, traits=None, var_convent
     for jj, j in enumerate(traits):
         M = assemble_covariance(Phi, float(sigma2[j]), float(h2[j]))     # line 1
         L = cholesky_lower(M)                                           # line 2
-        XLw = forward_substitute(L, XL)                                 # line 3 (X_L part of every X_i)
         yw = forward_substitute(L, Y[:, j])                             # line 4
         for c0 in range(0, ns, snp_chunk):
             c1 = min(ns, c0 + snp_chunk)
-            gw = forward_substitute(L, G[:, c0:c1].astype(np.float64))  # line 3 (g_i part of X_i)
+            # line 3 on [X_L | g_c0 .. g_c1-1]: the X_L part of every X_i and the SNP columns in one substitution
+            # (>= 2 right-hand sides, like gls_single's [X_L | g_i]: every column takes the same arithmetic path)
+            Xc = forward_substitute(L, np.column_stack([XL, G[:, c0:c1].astype(np.float64)]))
             k = c1 - c0
             Xw = np.empty((k, n, w))                                    # X_i := L^-1 X_i for each i
-            Xw[:, :, :p] = XLw[None, :, :]
-            Xw[:, :, p] = gw.T
-            S = np.einsum("kna,knb->kab", Xw, Xw)                       # line 5
-            r = np.einsum("kna,n->ka", Xw, yw)                          # line 6
+            Xw[:, :, :p] = Xc[None, :, :p]
+            Xw[:, :, p] = Xc[:, p:].T
+            S, r = normal_equations(Xw, yw)                             # lines 5-6
             bb, VV, st = _finish(S, r, np.full(k, float(sigma2[j])), eps_collinear, var_convention)  # line 7
             b[c0:c1, jj] = bb
             Var[c0:c1, jj] = VV

@@ -207,15 +207,22 @@ def _small_cfg_data(n=48, p=4, m=37, t=5, seed_index=101):
     return cfg, ds, XR
 
 
-def test_sequence_matches_single_per_pair():
-    cfg, ds, XR = _small_cfg_data()
-    out = oracle.gls_sequence(ds.Phi, ds.XL, XR, ds.Y, ds.h2, ds.s2)
-    for i in [0, 5, 36]:
+@pytest.mark.parametrize("p,chunk", [(4, 4096), (4, 7), (1, 5)])
+def test_sequence_matches_single_per_pair(p, chunk):
+    """the trait-cached sequence is BITWISE equal to the literal per-pair Alg. 1 (gls_single, which
+    re-assembles and re-factors M_j for every pair), for every pair, including collinear (NaN-payload) pairs and
+    chunk boundaries."""
+    cfg, ds, XR = _small_cfg_data(p=p)
+    XR = XR.copy()
+    XR[:, 7] = 0.0                       # monomorphic SNP: collinear with the intercept (status 1)
+    out = oracle.gls_sequence(ds.Phi, ds.XL, XR, ds.Y, ds.h2, ds.s2, snp_chunk=chunk)
+    assert out["status"][7].tolist() == [oracle.STATUS_COLLINEAR] * cfg.t
+    for i in range(cfg.m):
         for j in range(cfg.t):
             b, V, st = oracle.gls_single(ds.Phi, np.column_stack([ds.XL, XR[:, i]]), ds.Y[:, j], ds.s2[j], ds.h2[j])
             assert st == out["status"][i, j]
-            np.testing.assert_allclose(out["b"][i, j], b, rtol=1e-12, atol=1e-12)
-            np.testing.assert_allclose(out["Var"][i, j], V, rtol=1e-12, atol=1e-14)
+            np.testing.assert_array_equal(out["b"][i, j], b)
+            np.testing.assert_array_equal(out["Var"][i, j], V)
 
 
 def test_p10_identical_traits_and_slices():
