@@ -241,10 +241,20 @@ def xr_columns(cfg: Config, snps) -> np.ndarray:
     """Selected X_R columns as float64 (n, len(snps)), regenerating only the blocks they live in."""
     snps = np.asarray(snps, dtype=np.int64)
     out = np.empty((cfg.n, snps.size), dtype=np.float64)
-    blocks = {}
+    by_block = {}
     for idx, s in enumerate(snps):
-        b = int(s) // GEN_BLOCK
-        if b not in blocks:
-            blocks[b] = snp_block(cfg, b)
-        out[:, idx] = blocks[b][int(s) - b * GEN_BLOCK]
+        by_block.setdefault(int(s) // GEN_BLOCK, []).append(idx)
+
+    def work(b):
+        g = snp_block(cfg, b)
+        for idx in by_block[b]:
+            out[:, idx] = g[int(snps[idx]) - b * GEN_BLOCK]
+
+    nthr = min(16, os.cpu_count() or 1, max(1, len(by_block)))
+    if nthr == 1:
+        for b in by_block:
+            work(b)
+    else:
+        with _cf.ThreadPoolExecutor(nthr) as ex:
+            list(ex.map(work, list(by_block)))
     return out

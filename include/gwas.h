@@ -82,7 +82,10 @@ typedef struct {
   int32_t xr_dtype;        /* GWAS_XR_F64 or GWAS_XR_U8 */
   int32_t output_mode;     /* GWAS_OUT_SNP (default) or GWAS_OUT_FULL */
   int32_t var_convention;  /* GWAS_VAR_TEXTBOOK (default) or GWAS_VAR_LITERAL */
-  int64_t block_cols;      /* SNP columns per streamed block k ("user-configurable"); default 8192 */
+  int64_t block_cols;      /* SNP columns per streamed block k ("user-configurable"); default 8192.
+                              0 = auto: FP64 mode picks the k in [4096, 16384] (multiple of 128) whose K1 / K2 tile
+                              grids quantise best into whole waves on the device's SMs (int8-sliced mode: 8192);
+                              gwas_run_info reports the choice.  Results are bitwise independent of k. */
   double eps_spd;          /* default 1e-10 */
   double eps_collinear;    /* default 1e-10, relative Schur-complement threshold (reading A6) */
   void* compute_stream;    /* cudaStream_t for kernels (NULL = legacy default stream) */
@@ -165,6 +168,14 @@ GWAS_API gwas_status gwas_setup_estimate(const gwas_options* opt, int64_t n, int
 /* Low-rank trait weights chosen at setup: *r = kept rank (0 = exact weights), *s0 / *s_r = largest singular value
  * of D and the first dropped one (either may be NULL). */
 GWAS_API gwas_status gwas_trait_rank(gwas_ctx* ctx, int32_t* r, double* s0, double* s_r);
+
+/* Estimation diagnostics: g_star[j] = index g of the first grid maximum h = g/100 of trait j's profile likelihood
+ * (reading E3), t int32 values written to host memory.  GWAS_E_STATE for a context not made by gwas_setup_estimate. */
+GWAS_API gwas_status gwas_estimate_grid_argmax(gwas_ctx* ctx, int32_t* g_star);
+
+/* Run configuration fixed at setup / attach: *block_cols = k actually used (resolves block_cols = 0), *fused_k2 =
+ * 1 if K2 is contracted in K1's epilogue for this shape (opt.fuse_k2 and few traits).  Either may be NULL. */
+GWAS_API gwas_status gwas_run_info(gwas_ctx* ctx, int64_t* block_cols, int32_t* fused_k2);
 
 /* Event time (ms) of the estimation kernels of gwas_setup_estimate (0 for a gwas_setup context). */
 GWAS_API gwas_status gwas_estimate_ms(gwas_ctx* ctx, double* ms);

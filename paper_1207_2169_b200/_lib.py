@@ -19,7 +19,7 @@ ALG_EIG, ALG_CHOL = 0, 1
 EST_ML, EST_REML = 0, 1
 NUM_TIMERS = 4
 
-EXPORTS = ["gwas_default_options", "gwas_state_bytes", "gwas_workspace_bytes", "gwas_setup", "gwas_setup_estimate", "gwas_estimate_ms", "gwas_trait_rank", "gwas_attach",
+EXPORTS = ["gwas_default_options", "gwas_state_bytes", "gwas_workspace_bytes", "gwas_setup", "gwas_setup_estimate", "gwas_estimate_ms", "gwas_trait_rank", "gwas_run_info", "gwas_estimate_grid_argmax", "gwas_attach",
            "gwas_run", "gwas_timings", "gwas_kernel_times", "gwas_gemm_tn", "gwas_destroy", "gwas_last_error",
            "gwas_version"]
 
@@ -54,6 +54,8 @@ def _load():
         "gwas_setup_estimate": (C.c_int, [opt, i64, i64, i64, P, P, P, i32, P, P, P, P, sz, P, sz, C.POINTER(P)]),
         "gwas_estimate_ms": (C.c_int, [P, dp]),
         "gwas_trait_rank": (C.c_int, [P, C.POINTER(C.c_int32), dp, dp]),
+        "gwas_run_info": (C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+        "gwas_estimate_grid_argmax": (C.c_int, [P, C.POINTER(C.c_int32)]),
         "gwas_attach": (C.c_int, [opt, i64, i64, i64, P, sz, P, sz, C.POINTER(P)]),
         "gwas_run": (C.c_int, [P, i64, P, i64, P, P, P]),
         "gwas_timings": (C.c_int, [P, dp, dp, dp]),

@@ -104,7 +104,7 @@ class Gwas:
 
     def setup_estimate(self, Phi, XL, Y, method: str = "reml"):
         """The paper's first step + setup: estimate (h2_j, sigma2_j) per trait by ML / REML in the
-        eigenbasis, then precompute with them.  Returns dict(h2, sigma2, loglik) as float64 numpy arrays (t,)."""
+        eigenbasis, then precompute with them.  Returns dict(h2, sigma2, loglik) as float64 numpy arrays (t,) and g_star (int32, the first grid argmax)."""
         self._close_ctx()
         phi = _colmajor_f64(Phi)
         xl = _colmajor_f64(XL)
@@ -120,13 +120,21 @@ class Gwas:
                                           _EST[method], h2.ctypes.data, s2.ctypes.data, ll.ctypes.data,
                                           self.state.data_ptr(), self.state_bytes, self.work.data_ptr(),
                                           self.work_bytes, C.byref(self._ctx)))
-        return {"h2": h2, "sigma2": s2, "loglik": ll}
+        gs = np.empty(self.t, dtype=np.int32)
+        check(lib.gwas_estimate_grid_argmax(self._ctx, gs.ctypes.data_as(C.POINTER(C.c_int32))))
+        return {"h2": h2, "sigma2": s2, "loglik": ll, "g_star": gs}
 
     def trait_rank(self):
         """(r, s0, s_r): the low-rank trait-weight rank chosen at setup (0 = exact weights) and the singular values."""
         r, s0, sr = C.c_int32(), C.c_double(), C.c_double()
         check(lib.gwas_trait_rank(self._ctx, C.byref(r), C.byref(s0), C.byref(sr)))
         return r.value, s0.value, sr.value
+
+    def run_info(self):
+        """{"block_cols": k used by gwas_run (resolves block_cols=0, auto), "fused_k2": K2 in K1's epilogue}."""
+        k, f = C.c_int64(), C.c_int32()
+        check(lib.gwas_run_info(self._ctx, C.byref(k), C.byref(f)))
+        return {"block_cols": k.value, "fused_k2": bool(f.value)}
 
     def estimate_ms(self) -> float:
         ms = C.c_double()

@@ -7,6 +7,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -106,7 +107,7 @@ Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   d.n2 = d.nsq + t;
   d.ldc2 = round_up(d.n2, 2);
   d.lds = round_up(t * (p + 1), 2);
-  d.kb = o->block_cols > 0 ? o->block_cols : 8192;
+  d.kb = o->block_cols > 0 ? o->block_cols : 8192;  // 0 (auto): set below, once the product shapes are known
   d.es = o->xr_dtype == GWAS_XR_U8 ? 1 : 8;
   d.i8 = o->int8_slices != 0;
   d.per_pair = o->output_mode == GWAS_OUT_FULL ? p + 1 : 1;
@@ -362,6 +363,20 @@ gwas_status make_map(CUtensorMap* map, const void* ptr, bool u8, int64_t K, int6
   return GWAS_OK;
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device (per-context) setting: remember, per kernel
+// instantiation, the devices it has been set on (bit d of `mask`).  Setting it twice (two threads racing on a
+// fresh device) is harmless: the call is idempotent.
+template <typename Kern>
+gwas_status ensure_smem_attr(Kern kern, size_t smem, std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  CKC(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return GWAS_OK;
+  CKC(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return GWAS_OK;
+}
+
 constexpr int kBM = 128;
 constexpr int kStagesU8 = 8, kStagesF64 = 6, kStagesF64N64 = 8;
 
@@ -373,20 +388,94 @@ constexpr size_t gemm_smem_bytes() {
 
 template <typename TA, int BN, int STAGES, bool SQ, bool FUSE = false>
 gwas_status launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const gw::GemmShape& s, cudaStream_t st) {
-  static bool attr_set = false;  // per instantiation (the library binds one device per process)
+  static std::atomic<uint64_t> attr_devs{0};  // per instantiation, per device
   constexpr size_t smem = gemm_smem_bytes<TA, BN, STAGES>();
   static_assert(!FUSE || (size_t)((BN / 32) * kBM + BN) * gw::FUSE_MAX_NQ * 8 <=
                              (size_t)STAGES * (gw::GemmSmem<TA, kBM, BN>::kAStride + gw::GemmSmem<TA, kBM, BN>::kBStride),
                 "fused-K2 reduction buffer must fit in the stage buffers");
   auto kern = gw::gemm_tn_dmma<TA, kBM, BN, STAGES, SQ, FUSE>;
-  if (!attr_set) {
-    CKC(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  CKG(ensure_smem_attr(kern, smem, attr_devs));
   const int grid = s.tiles_m * s.tiles_n * s.ksplit;
   kern<<<grid, gw::GEMM_THREADS, smem, st>>>(ma, mb, s);
   CKC(cudaGetLastError());
   return GWAS_OK;
+}
+
+// Output-tile width (128 or 64 columns) of the DMMA kernel for an M x N product.
+//   - 64 wide when 128 x 128 tiles would give fewer than 4 waves on 148 SMs (e.g. K2b, N = t): the wave tail
+//     dominates there, not the extra fragment loads of the narrower warp tiles (GWAS_BN64_WAVES overrides the
+//     4-wave threshold; 0 = always 128 wide; tuning knob).
+//   - fp64 A (one CTA per SM either way): whole waves compared, a 64-wide tile doing half the work of a 128-wide
+//     one at ~93 % of its efficiency (measured on K2b, C4: 5.36 ms at 128 vs 5.04 ms at 64 wide).
+//   - fused K2: the per-tile partials are summed over the column tiles, so the tile width fixes the rounding of the
+//     K2 terms.  It is chosen from N alone -- the width a full 8192-column block would get -- so results stay bitwise
+//     invariant to the block size and to shard edges (a short tail block gets the same tiles).
+//   - wide_split (medium-width fp64 products with a long K: the int8 mode's K2b at t <= 1024, n >= 4096): 128-wide
+//     tiles split 2-way along K (fixed halves, chosen from N and K only) instead of 64-wide tiles.
+int bn64_waves() {
+  static const int w = [] {
+    const char* e = getenv("GWAS_BN64_WAVES");
+    return e ? atoi(e) : 4;
+  }();
+  return w;
+}
+
+int choose_bn(bool a_u8, int64_t M, int64_t N, bool fuse, bool wide_split) {
+  if (wide_split) return 128;
+  if (N <= 64) return 64;
+  if (fuse) return (8192 / kBM) * ((N + 127) / 128) < (int64_t)bn64_waves() * 148 ? 64 : 128;
+  const int64_t tiles128 = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
+  if (!a_u8 && !getenv("GWAS_BN64_WAVES")) {
+    const int64_t tiles64 = ((M + kBM - 1) / kBM) * ((N + 63) / 64);
+    const double cost128 = (double)((tiles128 + 147) / 148), cost64 = (double)((tiles64 + 147) / 148) * 0.5 / 0.93;
+    return cost64 < cost128 ? 64 : 128;
+  }
+  return tiles128 < (int64_t)bn64_waves() * 148 ? 64 : 128;
+}
+
+// Relative time of one M-row DMMA product of width N on `sms` SMs: whole waves of CTAs, a wave costing the CTA slots
+// it occupies (a 64-wide tile is half a 128-wide one, at ~93 % of its efficiency; u8-A 64-wide tiles run two per SM).
+double dmma_wave_cost(bool a_u8, int64_t M, int64_t N, bool fuse, int sms) {
+  const int bn = choose_bn(a_u8, M, N, fuse, false);
+  const int per_sm = (a_u8 && bn == 64) ? 2 : 1;
+  const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + bn - 1) / bn);
+  const int64_t slots = (int64_t)sms * per_sm;
+  const double waves = (double)((tiles + slots - 1) / slots);
+  return waves * (double)slots * bn / 128.0 / (double)per_sm / (bn == 64 ? 0.93 : 1.0);
+}
+
+// block_cols = 0 (auto): the k in [4096, 16384] (a multiple of 128) that minimises the wave-quantised time per SNP
+// column of the block's DMMA products -- K1 (M = k, N = n, u8 or fp64 A, with K2 fused when it is) and the unfused
+// K2 (M = k, N = t(p+2) rounded as in the state, fp64 A) -- both with K = n.  Ties go to the k closest to 8192.
+// The int8-sliced mode keeps 8192.  Results do not depend on k (fixed K order, no split chosen from M).
+int64_t auto_block_cols(const Dims& d, const gwas_options* o) {
+  if (d.i8) return 8192;
+  int sms = 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o->device) != cudaSuccess || sms <= 0) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  const bool u8 = d.es == 1;
+  int64_t best = 8192;
+  double best_cost = 1e300;
+  for (int64_t k = 4096; k <= 16384; k += kBM) {
+    double cost = dmma_wave_cost(u8, k, d.n, d.fuse, sms);
+    if (!d.fuse) cost += dmma_wave_cost(false, k, d.n2, false, sms);
+    cost /= (double)k;
+    const bool better = cost < best_cost * (1.0 - 1e-9) ||
+                        (cost <= best_cost * (1.0 + 1e-9) && std::llabs(k - 8192) < std::llabs(best - 8192));
+    if (better) {
+      best = k;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+Dims make_dims_kb(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
+  Dims d = make_dims(n, p, t, o);
+  if (o->block_cols == 0) d.kb = auto_block_cols(d, o);
+  return d;
 }
 
 // C[M x N] (row-major, ldc) = A[M x K] (rows K-contiguous, lda) * B[N x K]^T (rows K-contiguous, ldb)
@@ -408,24 +497,9 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   // 128 x 64 tiles when 128 x 128 tiles would give fewer than 4 waves on 148 SMs (e.g. K2b, N = t):
   // the wave tail dominates there, not the extra fragment loads of the narrower warp tiles
   // GWAS_BN64_WAVES overrides the 4-wave threshold (0 = always 128 wide; tuning knob).
-  static int bn64_waves = [] {
-    const char* e = getenv("GWAS_BN64_WAVES");
-    return e ? atoi(e) : 4;
-  }();
-  const int64_t tiles128 = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
-  int bn = (N <= 64 || tiles128 < (int64_t)bn64_waves * 148) ? 64 : 128;
-  if (!a_u8 && N > 64 && !getenv("GWAS_BN64_WAVES")) {
-    // fp64 A (one CTA per SM either way): compare whole waves, a 64-wide tile doing half the work of a 128-wide
-    // one at ~93 % of its efficiency (measured on K2b, C4: 5.36 ms at 128 vs 5.04 ms at 64 wide)
-    const int64_t tiles64 = ((M + kBM - 1) / kBM) * ((N + 63) / 64);
-    const double cost128 = (double)((tiles128 + 147) / 148), cost64 = (double)((tiles64 + 147) / 148) * 0.5 / 0.93;
-    bn = cost64 < cost128 ? 64 : 128;
-  }
-  // Medium-width fp64 products with a long K (int8 mode's K2b at t <= 1024, n >= 4096): 128-wide tiles split 2-way
-  // along K (fixed halves, chosen from N and K only: bitwise invariant to the block size) instead of 64-wide tiles
   const int kt_all0 = (int)((K + gw::GEMM_BK - 1) / gw::GEMM_BK);
   const bool wide_split = wide_split_scratch && !fuse && !a_u8 && N > 64 && N <= kWideSplitN && kt_all0 >= 256;
-  if (wide_split) bn = 128;
+  const int bn = choose_bn(a_u8, M, N, fuse, wide_split);
   CUtensorMap ma, mb;
   CKG(make_map(&ma, A, a_u8, K, M, lda, kBM));
   CKG(make_map(&mb, B, false, K, N, ldb, bn));
@@ -560,13 +634,10 @@ template <int S>
 gwas_status launch_i8_s(int CL, const CUtensorMap& ma, const CUtensorMap& mb, const gw::I8Shape& s, unsigned grid,
                         cudaStream_t st) {
   constexpr size_t smem = gw::I8Cfg<S>::smem_bytes(gw::I8_EPI_SMEM);
-  static bool attr_set = false;
-  if (!attr_set) {
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<1, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<2, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced<4, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr1{0}, attr2{0}, attr4{0};
+  CKG(ensure_smem_attr(gw::gemm_i8_sliced<1, S>, smem, attr1));
+  CKG(ensure_smem_attr(gw::gemm_i8_sliced<2, S>, smem, attr2));
+  CKG(ensure_smem_attr(gw::gemm_i8_sliced<4, S>, smem, attr4));
   if (CL == 1) {
     gw::gemm_i8_sliced<1, S><<<grid, gw::I8_THREADS, smem, st>>>(ma, mb, s);
     CKC(cudaGetLastError());
@@ -649,11 +720,8 @@ gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, c
   if (two_sm) {
     constexpr size_t smem2 =
         1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256 + gw::I8_EPI_SMEM;
-    static bool attr2 = false;
-    if (!attr2) {
-      CKC(cudaFuncSetAttribute(gw::gemm_i8_sliced_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      attr2 = true;
-    }
+    static std::atomic<uint64_t> attr_2sm{0};
+    CKG(ensure_smem_attr(gw::gemm_i8_sliced_2sm, smem2, attr_2sm));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(gw::I8_THREADS);
@@ -732,6 +800,7 @@ struct gwas_ctx {
   int stage_next = 0;
   bool stage_zeroed = false;
   float ms_eig = 0.f, ms_pre = 0.f, ms_est = 0.f;
+  std::vector<int32_t> est_gstar;  // estimation: first grid argmax per trait (reading E3), copied at setup
   // per-kernel event timers
   struct Pending {
     int kind;
@@ -868,13 +937,13 @@ const char* gwas_version(void) {
 
 size_t gwas_state_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   if (check_sizes(n, p, t, o) != GWAS_OK) return 0;
-  Dims d = make_dims(n, p, t, o);
+  Dims d = make_dims_kb(n, p, t, o);
   return (size_t)make_header(d, o).total;
 }
 
 size_t gwas_workspace_bytes(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   if (check_sizes(n, p, t, o) != GWAS_OK) return 0;
-  Dims d = make_dims(n, p, t, o);
+  Dims d = make_dims_kb(n, p, t, o);
   int64_t lwork = 0;
   size_t host_ws = 0;
   if (solver_lwork(o, n, d.kpad, &lwork, &host_ws) != GWAS_OK) return 0;
@@ -899,7 +968,7 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
     return fail(GWAS_E_ARG, "NULL pointer argument");
   *out = nullptr;
   CKC(cudaSetDevice(o->device));
-  Dims d = make_dims(n, p, t, o);
+  Dims d = make_dims_kb(n, p, t, o);
   StateHeader h = make_header(d, o);
   int64_t lwork = 0;
   size_t host_ws = 0;
@@ -1156,6 +1225,8 @@ gwas_status setup_impl(const gwas_options* o, int64_t n, int64_t p, int64_t t, c
       if (h2_out) CKC(cudaMemcpy(h2_out, dh2, sizeof(double) * t, cudaMemcpyDefault));
       if (s2_out) CKC(cudaMemcpy(s2_out, ds2, sizeof(double) * t, cudaMemcpyDefault));
       if (ll_out) CKC(cudaMemcpy(ll_out, w + sl.est_ll, sizeof(double) * t, cudaMemcpyDefault));
+      c->est_gstar.resize(t);
+      CKC(cudaMemcpy(c->est_gstar.data(), w + sl.est_gs, sizeof(int32_t) * t, cudaMemcpyDeviceToHost));
     }
     float ms_all = 0.f, ms_eig = 0.f;
     CKC(cudaEventElapsedTime(&ms_all, e0, e3));
@@ -1221,6 +1292,22 @@ gwas_status gwas_trait_rank(gwas_ctx* c, int32_t* r, double* s0, double* s_r) {
   return GWAS_OK;
 }
 
+gwas_status gwas_run_info(gwas_ctx* c, int64_t* block_cols, int32_t* fused_k2) {
+  g_err.clear();
+  if (!c) return fail(GWAS_E_STATE, "NULL context");
+  if (block_cols) *block_cols = c->d.kb;
+  if (fused_k2) *fused_k2 = c->d.fuse ? 1 : 0;
+  return GWAS_OK;
+}
+
+gwas_status gwas_estimate_grid_argmax(gwas_ctx* c, int32_t* g_star) {
+  g_err.clear();
+  if (!c || !g_star) return fail(GWAS_E_ARG, "NULL argument");
+  if (c->est_gstar.size() != (size_t)c->d.t) return fail(GWAS_E_STATE, "context was not created by gwas_setup_estimate");
+  std::copy(c->est_gstar.begin(), c->est_gstar.end(), g_star);
+  return GWAS_OK;
+}
+
 gwas_status gwas_estimate_ms(gwas_ctx* c, double* ms) {
   g_err.clear();
   if (!c || !ms) return fail(GWAS_E_ARG, "NULL argument");
@@ -1235,7 +1322,7 @@ gwas_status gwas_attach(const gwas_options* o, int64_t n, int64_t p, int64_t t, 
   if (!out || !state_dev || !work_dev) return fail(GWAS_E_ARG, "NULL pointer argument");
   *out = nullptr;
   CKC(cudaSetDevice(o->device));
-  Dims d = make_dims(n, p, t, o);
+  Dims d = make_dims_kb(n, p, t, o);
   StateHeader want = make_header(d, o);
   if (state_bytes < (size_t)want.total) return fail(GWAS_E_NOMEM, "state buffer too small");
   RunLayout rl = run_layout(d, o->overlap != 0);

@@ -33,7 +33,31 @@ def test_bench_json_line_config0():
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
     assert d["parity"]["pass"] and d["modes"]["int8_sliced"]["parity"]["pass"]
+    assert d["parity"]["e2e_host"]["pass"] and d["parity"]["pairs"] >= 8000   # all 2000 SNPs x 4 traits
     assert "estimate" in d["modes"]
+    assert d["config"]["shards"] == [[0, 2000]] and d["scaling"] == "strong"
+    assert d["cpu_baseline"]["literal"]["value"] > 0
+
+
+def test_bench_self_launches_n_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks (here over gloo on the one GPU;
+    NCCL needs one GPU per rank) and checks a parity subsample cut from EVERY rank's shard."""
+    pytest.importorskip("torch")
+    env = dict(os.environ, GWAS_BENCH_BACKEND="gloo")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "0", "--steps", "1", "--warmup", "3",
+                          "--no-cpu-baseline", "--no-est-alt"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["shards"] == [[0, 1000], [1000, 2000]]
+    assert d["parity"]["pass"] and [r["rank"] for r in d["parity"]["per_rank"]] == [0, 1]
+    assert all(r["pairs"] >= 4000 for r in d["parity"]["per_rank"])
+    assert d["modes"]["int8_sliced"]["parity"]["pass"]
+    assert len(d["ranks"]) == 2
 
 
 def test_bench_two_ranks_gloo_on_one_gpu():
@@ -53,3 +77,4 @@ def test_bench_two_ranks_gloo_on_one_gpu():
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "snp-shard x2"
     assert d["setup"]["broadcast_bytes"] > 0 and d["parity"]["pass"]
     assert d["modes"]["int8_sliced"]["parity"]["pass"]
+    assert [r["rank"] for r in d["parity"]["per_rank"]] == [0, 1]   # rank 1's shard is checked too

@@ -1,6 +1,8 @@
 """GPU parity at BASELINE.json's full sizes (configs 1-4), in the launch configuration bench.py times
-(uint8 X_R resident in HBM, k = 8192 blocks), checked on the seeded stratified subsample of reading A18
-(>= 10^4 pairs: <= 16 traits incl. 0 and t-1, SNPs incl. 0, m-1 and block edges) against the CPU oracle."""
+(uint8 X_R resident in HBM; FP64 mode: blocks pipelined over two streams (overlap) with the auto block size, the
+headline; int8 mode: overlap, k = 8192), checked on the seeded stratified subsample of reading A18 (>= 10^4 pairs:
+<= 16 traits incl. 0 and t-1, SNPs incl. 0, m-1 and the block edges of the k actually used) against the CPU
+oracle."""
 import numpy as np
 import pytest
 
@@ -24,12 +26,15 @@ def test_full_config_subsample(index, i8, lr):
     xr = torch.empty((cfg.m, ld), dtype=torch.uint8, pin_memory=True)
     datagen.xr_dosages(cfg, ld=ld, out=xr.numpy())
     xr_dev = xr.to(dev)
-    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=8192, int8_slices=i8, trait_rank=lr)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=0 if (i8 == 0 and lr == 0) else 8192, int8_slices=i8,
+                  trait_rank=lr, overlap=True)
     eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
     rank = eng.trait_rank()[0]
     assert (rank > 0) == (lr != 0)  # C2 / C4 (t = 1000) compress
+    k = eng.run_info()["block_cols"]
     b, v, s = eng.run(xr_dev)
-    snps, traits = datagen.subsample(cfg)
+    last = (cfg.m - 1) // k * k
+    snps, traits = datagen.subsample(cfg, forced_snps=[k - 1, k, 2 * k - 1, last - 1, last])
     idx_s = torch.from_numpy(snps).to(dev)
     idx_t = torch.from_numpy(traits).to(dev)
     bs = b.index_select(0, idx_s).index_select(1, idx_t).cpu().numpy()
@@ -41,7 +46,7 @@ def test_full_config_subsample(index, i8, lr):
     G = datagen.xr_columns(cfg, snps)
     ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
     eb, ev = compare(bs, vs, ss, ref)
-    print(f"C{index} int8_slices={i8} trait_rank={rank}: {snps.size} SNPs x {traits.size} traits = {snps.size * traits.size} pairs, "
+    print(f"C{index} int8_slices={i8} trait_rank={rank} k={k}: {snps.size} SNPs x {traits.size} traits = {snps.size * traits.size} pairs, "
           f"max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
     assert snps.size * traits.size >= 10_000
     assert eb <= TOL_B and ev <= TOL_VAR

@@ -5,7 +5,7 @@ Tolerances (derived in DESIGN.md §6d): the estimate h2^ is a root of dl/dh loca
 derivative's rounding noise (~1e-13 relative to its terms) over its slope (~n) moves the root by < 1e-11, so
 |h2_gpu - h2_ref| <= 1e-8 absolute, sigma2 relative <= 1e-8, log-likelihood relative <= 1e-10.  Where the two sides'
 first grid maxima differ (a near-tie of two grid likelihoods), the tie itself is checked instead (<= 1e-9 relative)
-and the trait is excluded from the h2 comparison.  End to end, (b, Var) after estimation match the oracle's GLS
+and the trait is excluded from the h2 comparison -- at most 1 % of the traits (see _check).  End to end, (b, Var) after estimation match the oracle's GLS
 evaluated at the oracle's own estimates within the north-star tolerances.
 """
 import numpy as np
@@ -35,19 +35,30 @@ def _ld(n, es=1):
 
 
 def _check(ds, method, gpu, ref, traits):
-    """Compare GPU estimates (all traits) with oracle estimates on `traits`; returns max errors.  A trait whose
-    h2 differs by more than TOL_H2 must be an equally good maximiser (two grid maxima tied): the oracle's
-    likelihood at the GPU's h2 is then within 1e-9 relative of the oracle's optimum, and it is skipped."""
+    """Compare GPU estimates (all traits) with oracle estimates on `traits`; returns max errors.
+
+    A trait whose h2 differs by more than TOL_H2 is excluded from the h2 comparison only when it is a genuine near-tie
+    of two grid likelihoods: the two sides' first grid argmaxes differ (GPU g_star from gwas_estimate_grid_argmax vs
+    the oracle's), the oracle's likelihood at the GPU's h2 is within 1e-9 relative of the oracle's optimum, and the
+    GPU's sigma2 and log-likelihood equal the oracle's evaluated AT the GPU's h2 (sigma2 rel <= 1e-8, ll rel <= 1e-10).
+    At most 1 % of the compared traits (rounded down) may be excluded, so a broken estimator cannot pass by exclusion."""
     meth = OE.REML if method == "reml" else OE.ML
     eh = es = el = 0.0
+    skipped = []
     for jj, j in enumerate(traits):
         if abs(gpu["h2"][j] - ref["h2"][jj]) > TOL_H2:
-            alt = OE.profile_loglik(ds.Phi, ds.XL, ds.Y[:, j], gpu["h2"][j], meth)["ll"]
-            assert abs(alt - ref["ll"][jj]) <= 1e-9 * abs(ref["ll"][jj]), (j, gpu["h2"][j], ref["h2"][jj])
+            assert int(gpu["g_star"][j]) != int(ref["g_star"][jj]), \
+                (j, gpu["h2"][j], ref["h2"][jj], "same grid argmax: not a tie")
+            alt = OE.profile_loglik(ds.Phi, ds.XL, ds.Y[:, j], gpu["h2"][j], meth)
+            assert abs(alt["ll"] - ref["ll"][jj]) <= 1e-9 * abs(ref["ll"][jj]), (j, gpu["h2"][j], ref["h2"][jj])
+            assert abs(gpu["sigma2"][j] - alt["sigma2"]) <= TOL_S2 * alt["sigma2"], j
+            assert abs(gpu["loglik"][j] - alt["ll"]) <= TOL_LL * abs(alt["ll"]), j
+            skipped.append(int(j))
             continue
         eh = max(eh, abs(gpu["h2"][j] - ref["h2"][jj]))
         es = max(es, abs(gpu["sigma2"][j] - ref["sigma2"][jj]) / ref["sigma2"][jj])
         el = max(el, abs(gpu["loglik"][j] - ref["ll"][jj]) / abs(ref["ll"][jj]))
+    assert len(skipped) <= int(0.01 * len(traits)), f"near-tie exclusions {skipped} exceed 1% of {len(traits)} traits"
     return eh, es, el
 
 
