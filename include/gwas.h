@@ -37,6 +37,8 @@
  *   GWAS_I8_TRACE=<file>    append %globaltimer phase stamps of the int8 kernel to <file> (allocates a 256 KB
  *                           device buffer and synchronises after every launch)
  *   GWAS_I8_DBG=1|2         int8 epilogue without TMEM loads / stores (timing experiments; results invalid)
+ *   GWAS_K3_PLAIN=1         K3 on the trait-tiled C with the register-prefetch kernel instead of the bulk-copy
+ *                           (TMA) streamed one (comparison only; bitwise identical results)
  *   GWAS_LR_UNFUSED=1       low-rank mode: separate K = r recombination products + K3 instead of the fused kernel
  *                           (even t only; results equal up to rounding) */
 #ifndef GWAS_H

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgwas.so")
 SOURCES = ["gwas.cu", "est_p1_3.cu", "est_p4_6.cu", "est_p7_9.cu", "est_p10_12.cu"]
-HEADERS = ["estimate.cuh", "estimate_launch.cuh", "gemm_dmma.cuh", "gemm_i8.cuh", "lowrank_k3.cuh", "schur.cuh", "setup_kernels.cuh"]
+HEADERS = ["ctile.cuh", "estimate.cuh", "estimate_launch.cuh", "gemm_dmma.cuh", "gemm_i8.cuh", "lowrank_k3.cuh", "schur.cuh", "setup_kernels.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMPILE_FLAGS = ARCH + [

@@ -19,6 +19,8 @@
 
 #include <type_traits>
 
+#include "ctile.cuh"
+
 namespace gw {
 
 constexpr int GEMM_BK = 16;                 // K elements per stage (one 128-byte fp64 row)
@@ -46,6 +48,9 @@ struct GemmShape {
   int fnq, fnlin, fnsq;
   double* fP;
   long long fP_stride;  // doubles per tn
+  // C in the trait-tiled layout (ctile.cuh; K2 of the many-trait FP64 path): column col < cnlin is field col / ct,
+  // trait col % ct; columns [cnlin, nsq) are padding (not stored); col >= nsq is field cF - 1, trait col - nsq.
+  int ctiled, ct, cnlin, cF;
 };
 
 constexpr int FUSE_MAX_NQ = 28;  // fused K2 columns t (p + 2) per CTA: reduction buffer + operand slice fit the freed stages
@@ -371,6 +376,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, BN == 64 ? 2 : 1)
 #pragma unroll
       for (int w2 = 1; w2 < WARPS_N; ++w2) v += red[(long long)w2 * BM * nq + idx];
       P[(long long)(m0 + r) * nq + (idx - r * nq)] = v;
+    }
+  } else if (s.ctiled) {
+    // ---------------- epilogue, trait-tiled C: the lane's 2 NI column offsets are row-independent
+    // one integer division per thread: the warp's 32 columns span at most one field boundary (ct >= 32)
+    const int cw = n0 + wn * WN;
+    const int fb = min(cw, s.cnlin - 1) / s.ct;
+    long long coff[NI][2];
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = cw + j * 8 + 2 * q + e;
+        long long o = -1;
+        if (col < s.N) {
+          if (col < s.cnlin) {
+            const int f = fb + (col >= (fb + 1) * s.ct ? 1 : 0);
+            o = ctile_off(col - f * s.ct, f, s.cF);
+          } else if (col >= s.nsq) {
+            o = ctile_off(col - s.nsq, s.cF - 1, s.cF);
+          }
+        }
+        coff[j][e] = o;
+      }
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int row = m0 + wm * WM + i * 8 + g;
+      if (row >= s.M) continue;
+      double* crow = s.C + (long long)row * s.ldc;
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const long long o0 = coff[j][0], o1 = coff[j][1];
+        if (o0 >= 0 && o1 == o0 + 1 && !(o0 & 1)) {
+          *reinterpret_cast<double2*>(crow + o0) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else {
+          if (o0 >= 0) crow[o0] = acc[i][j][0];
+          if (o1 >= 0) crow[o1] = acc[i][j][1];
+        }
+      }
     }
   } else {
     // ---------------- epilogue: each lane owns C[row][2q, 2q+1] of every 8x8 fragment

@@ -64,6 +64,12 @@ gwas_status fail(gwas_status st, const char* fmt, ...) {
     if (g__ != GWAS_OK) return g__;         \
   } while (0)
 
+// Environment knob set to something other than "" / "0" (include/gwas.h lists the knobs).
+inline bool env_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] && !(e[0] == '0' && e[1] == 0);
+}
+
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline size_t align256(size_t a) { return (a + 255) / 256 * 256; }
 
@@ -94,6 +100,7 @@ struct Dims {
   bool lr;                         // low-rank trait weights requested (state reserves room; setup decides r)
   int64_t ldg2;                    // low-rank K2 output row stride (p rmax + t + 32 + rmax)
   bool fuse;                       // K2 fused into K1's epilogue (few traits, opt.fuse_k2)
+  bool ctiled;                     // K2 output C in the trait-tiled layout (ctile.cuh): FP64 exact weights, t >= 32
   int64_t fnq, ftiles;             // fused K2 columns per pair-row; max K1 column tiles (partials per block)
 };
 
@@ -121,6 +128,8 @@ Dims make_dims(int64_t n, int64_t p, int64_t t, const gwas_options* o) {
   d.fnq = d.i8 ? t : t * (p + 2);
   d.fuse = o->fuse_k2 != 0 && (d.i8 ? t <= gw::I8_FUSE_T : d.fnq <= gw::FUSE_MAX_NQ);
   d.ftiles = d.i8 ? d.na_pad / gw::I8_NB : (n + 63) / 64;
+  d.ctiled = !d.i8 && !d.lr && !d.fuse && t >= 32;
+  if (d.ctiled) d.ldc2 = gw::ctile_ld((int)t, (int)p + 2);
   return d;
 }
 
@@ -489,7 +498,8 @@ constexpr int kSplitMax = 8, kSplitLd = 64;
 gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                     int64_t M, int64_t N, int64_t K, int64_t nsq, cudaStream_t st, int group_m = 16,
                     double* split_scratch = nullptr, bool tri = false, const gw::GemmShape* fuse = nullptr,
-                    int* tiles_n_out = nullptr, double* wide_split_scratch = nullptr) {
+                    int* tiles_n_out = nullptr, double* wide_split_scratch = nullptr,
+                    const gw::GemmShape* ctile = nullptr) {
   if (M <= 0 || N <= 0) return GWAS_OK;
   if (K <= 0) return fail(GWAS_E_ARG, "gemm K = %lld", (long long)K);
   if ((ldc & 1) || (reinterpret_cast<uintptr_t>(C) & 15)) return fail(GWAS_E_ARG, "C not 16-byte aligned / ldc odd");
@@ -524,6 +534,15 @@ gwas_status gemm_tn(bool a_u8, const void* A, int64_t lda, const double* B, int6
   s.fnq = s.fnlin = s.fnsq = 0;
   s.fP = nullptr;
   s.fP_stride = 0;
+  s.ctiled = 0;
+  s.ct = s.cnlin = s.cF = 0;
+  if (ctile) {  // C in the trait-tiled layout (ctile.cuh); no split along K for these (wide) products
+    if (fuse || N <= kSplitLd || wide_split) return fail(GWAS_E_ARG, "trait-tiled C needs a plain wide product");
+    s.ctiled = 1;
+    s.ct = ctile->ct;
+    s.cnlin = ctile->cnlin;
+    s.cF = ctile->cF;
+  }
   if (fuse) {
     if (nsq < N || fuse->fnq > gw::FUSE_MAX_NQ || fuse->fnq < 1) return fail(GWAS_E_ARG, "bad fused-K2 shape");
     s.fB = fuse->fB;
@@ -605,9 +624,63 @@ gwas_status launch_lowrank_schur(const gw::LowrankK3Args& a, int p, cudaStream_t
   return GWAS_OK;
 }
 
+// K3 on the trait-tiled C: bulk-copy (TMA) streamed persistent kernel, one CTA per resident slot.  Two shapes
+// (measured per 15104-SNP C4 block / 8192-SNP block at n = 1e3, t = 1e4): 2 rows x 4 stages with the same row ranges
+// for every trait block when that fills >= 90 % of the CTA slots (C4: 0.178 ms, 6.2 TB/s), else 4 rows x 3 stages
+// over flattened trait-block-major ranges (t = 1e4: 0.99 ms, 6.0 TB/s).
+template <int P, int R, int ST>
+gwas_status launch_schur_tma_rs(const gw::SchurArgs& a, cudaStream_t st, bool need_aligned, bool* launched) {
+  constexpr size_t smem = gw::schur_tma_smem<P, R, ST>();
+  static std::atomic<uint64_t> attr_devs{0};
+  *launched = false;
+  CKG(ensure_smem_attr(gw::schur_solve_tma<P, R, ST>, smem, attr_devs));
+  int dev = 0, sms = 148, occ = 1;
+  CKC(cudaGetDevice(&dev));
+  CKC(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gw::schur_solve_tma<P, R, ST>, gw::CTILE_T, smem));
+  const int gx = (a.t + gw::CTILE_T - 1) / gw::CTILE_T;
+  const long long ntr = (a.cols + R - 1) / R;
+  const long long slots = (long long)std::max(occ, 1) * sms;
+  gw::SchurArgs b = a;
+  long long grid;
+  const long long gy = std::min<long long>(slots / gx, ntr);
+  if (gy >= 1 && gx * gy >= (slots * 9) / 10) {  // aligned row ranges fill >= 90 % of the CTA slots
+    b.k3_gy = (int)gy;
+    grid = gx * gy;
+  } else {
+    if (need_aligned) return GWAS_OK;
+    b.k3_gy = 0;
+    grid = std::max<long long>(1, std::min<long long>((long long)gx * ntr, slots));
+  }
+  gw::schur_solve_tma<P, R, ST><<<(unsigned)grid, gw::CTILE_T, smem, st>>>(b);
+  CKC(cudaGetLastError());
+  *launched = true;
+  return GWAS_OK;
+}
+
+template <int P>
+gwas_status launch_schur_tma(const gw::SchurArgs& a, cudaStream_t st) {
+  bool done = false;
+  CKG((launch_schur_tma_rs<P, 2, 4>(a, st, true, &done)));
+  if (!done) CKG((launch_schur_tma_rs<P, 4, 3>(a, st, false, &done)));
+  return GWAS_OK;
+}
+
 gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
   const long long np = (long long)a.cols * a.t;
   if (np == 0) return GWAS_OK;
+  static const bool k3_plain = env_flag("GWAS_K3_PLAIN");
+  if (a.tiled && !k3_plain) {
+    switch (p) {
+#define CASE_P(P) \
+  case P: return launch_schur_tma<P>(a, st);
+      CASE_P(1) CASE_P(2) CASE_P(3) CASE_P(4) CASE_P(5) CASE_P(6)
+      CASE_P(7) CASE_P(8) CASE_P(9) CASE_P(10) CASE_P(11) CASE_P(12)
+#undef CASE_P
+      default:
+        return fail(GWAS_E_ARG, "p = %d unsupported", p);
+    }
+  }
   const int threads = 128;
   gw::SchurArgs args = a;
   args.tj = 1;
@@ -1365,7 +1438,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
   const bool chol = c->opt.algorithm == GWAS_ALG_CHOL;
   const int64_t lr_r = c->h.lr_r, lr_nsq = c->h.lr_nsq, lr_nlin = c->h.lr_nlin;
   // low-rank: K3 fused with the K = r recombination (GWAS_LR_UNFUSED=1: separate products + K3, for comparison)
-  static const bool lr_unfused_env = getenv("GWAS_LR_UNFUSED") != nullptr;
+  static const bool lr_unfused_env = env_flag("GWAS_LR_UNFUSED");
   const bool lr_fused = lr_r > 0 && (!lr_unfused_env || (d.t & 1));  // the separate products need even t (alignment)
   const int64_t w = d.p + 1;
   const int64_t per_pair = c->opt.output_mode == GWAS_OUT_FULL ? w : 1;
@@ -1449,8 +1522,12 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
         if (!lr_fused) CKG(lowrank_recombine(c, g2, c2, cols, cs2));
       } else {
         static const int k2_group = getenv("GWAS_K2_GROUP") ? atoi(getenv("GWAS_K2_GROUP")) : 16;
+        gw::GemmShape ct{};
+        ct.ct = (int)d.t;
+        ct.cnlin = (int)(d.t * (d.p + 1));
+        ct.cF = (int)(d.p + 2);
         CKG(gemm_tn(false, xrp, d.kpad, c->B2(), d.kpad, c2, d.ldc2, cols, d.n2, d.n, d.nsq, cs2, k2_group,
-                    splitbuf));
+                    splitbuf, false, nullptr, nullptr, nullptr, d.ctiled ? &ct : nullptr));
       }
       CKG(c->toc(cs2));
     } else {
@@ -1502,6 +1579,7 @@ gwas_status gwas_run(gwas_ctx* c, int64_t ncols, const void* XR, int64_t ldx, do
     a.eps_collinear = c->opt.eps_collinear;
     a.literal = c->opt.var_convention == GWAS_VAR_LITERAL;
     a.full = c->opt.output_mode == GWAS_OUT_FULL;
+    a.tiled = (d.ctiled && lr_r == 0) ? 1 : 0;
     const int oset = (int)(bi & 1);
     uint8_t* ob = c->work + c->rl.outb[oset];
     if (out_dev) {
