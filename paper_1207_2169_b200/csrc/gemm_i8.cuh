@@ -149,13 +149,19 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
                : "r"(taddr));
 }
 
+// Debug trace (GWAS_I8_TRACE): 16 slots per CTA -- 0..6 %globaltimer phase stamps, 7 smid, 8 clock64 cycles the
+// MMA thread waited on full barriers, 9 cycles the producer waited on empty barriers, 10 k-stages.
+constexpr int I8_TRACE_SLOTS = 16;
 __device__ __forceinline__ void i8_stamp(const I8Shape& s, int slot) {
   if (s.trace && blockIdx.x < 4096) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    s.trace[blockIdx.x * 8 + slot] = globaltimer_ns();
-    s.trace[blockIdx.x * 8 + 7] = smid;
+    s.trace[blockIdx.x * I8_TRACE_SLOTS + slot] = globaltimer_ns();
+    s.trace[blockIdx.x * I8_TRACE_SLOTS + 7] = smid;
   }
+}
+__device__ __forceinline__ void i8_put(const I8Shape& s, int slot, unsigned long long v) {
+  if (s.trace && blockIdx.x < 4096) s.trace[blockIdx.x * I8_TRACE_SLOTS + slot] = v;
 }
 
 constexpr int EPI_CW = 8;  // output columns per TMEM drain chunk (S x 8 int32 registers in flight)
@@ -335,9 +341,14 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      unsigned long long wprod = 0;
       for (int kb = 0; kb < KB; ++kb) {
         const int st = kb % I8_STAGES;
-        if (kb >= I8_STAGES) mbar_wait(&empty[st], ((kb / I8_STAGES) - 1) & 1);
+        if (kb >= I8_STAGES) {
+          const long long c0 = s.trace ? clock64() : 0;
+          mbar_wait(&empty[st], ((kb / I8_STAGES) - 1) & 1);
+          if (s.trace) wprod += clock64() - c0;
+        }
         mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
         tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * I8_BKB, m0);
         if constexpr (CL == 1) {  // two boxes of BROWS/2 rows (the tensor map's box)
@@ -349,14 +360,18 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                          brow0 + (int)crank * QR, (uint16_t)((1u << CL) - 1));
         }
       }
+      i8_put(s, 9, wprod);
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_i8(256);               // digits 0..3 of the tile's 64 columns
       constexpr uint32_t idesc2 = idesc_i8((S - 4) * I8_NB);  // digits 4..S-1
+      unsigned long long wmma = 0;
       for (int kb = 0; kb < KB; ++kb) {
         const int st = kb % I8_STAGES;
+        const long long c0 = s.trace ? clock64() : 0;
         mbar_wait(&full[st], (kb / I8_STAGES) & 1);
+        if (s.trace && kb > 0) wmma += clock64() - c0;
         if (kb == 0) i8_stamp(s, 2);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t a0 = smem_u32(sA + st * A_BYTES);
@@ -376,6 +391,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       }
       umma_commit(tmem_full);     // accumulators complete
       i8_stamp(s, 3);
+      i8_put(s, 8, wmma);
+      i8_put(s, 10, KB);
     }
   } else if (warp >= 4) {
     i8_epilogue<S>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
@@ -491,9 +508,14 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      unsigned long long wprod = 0;
       for (int kb = 0; kb < KB; ++kb) {
         const int st = kb % I8_STAGES2;
-        if (kb >= I8_STAGES2) mbar_wait(&empty[st], ((kb / I8_STAGES2) - 1) & 1);
+        if (kb >= I8_STAGES2) {
+          const long long c0 = s.trace ? clock64() : 0;
+          mbar_wait(&empty[st], ((kb / I8_STAGES2) - 1) & 1);
+          if (s.trace) wprod += clock64() - c0;
+        }
         if (leader) mbar_expect_tx(&full[st], 2 * (A_BYTES + BH_BYTES));  // both CTAs' bytes land on it
         tma_load_2d_2sm(sA + st * A_BYTES, &tmA, &full[st], kb * I8_BKB, m0);
 #pragma unroll
@@ -501,13 +523,17 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
           tma_load_2d_2sm(sB + st * BH_BYTES + c * 128 * I8_BKB, &tmB, &full[st], kb * I8_BKB,
                           brow0 + c * 256 + (int)rank * 128);
       }
+      i8_put(s, 9, wprod);
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
       constexpr uint32_t idesc = idesc_i8_m256(256);
+      unsigned long long wmma = 0;
       for (int kb = 0; kb < KB; ++kb) {
         const int st = kb % I8_STAGES2;
+        const long long c0 = s.trace ? clock64() : 0;
         mbar_wait(&full[st], (kb / I8_STAGES2) & 1);
+        if (s.trace && kb > 0) wmma += clock64() - c0;
         if (kb == 0) i8_stamp(s, 2);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t a0 = smem_u32(sA + st * A_BYTES);
@@ -524,6 +550,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       }
       umma_commit_2sm(tmem_full);
       i8_stamp(s, 3);
+      i8_put(s, 8, wmma);
+      i8_put(s, 10, KB);
     }
   } else if (warp >= 4) {
     i8_epilogue<I8_SLICES>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);

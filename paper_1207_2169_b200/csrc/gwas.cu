@@ -778,9 +778,9 @@ gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, c
   // GWAS_I8_TRACE=<file>: debug phase stamps of the first 4096 CTAs of every launch, appended to <file>
   static const char* trace_path = getenv("GWAS_I8_TRACE");
   static unsigned long long* trace_dev = nullptr;
-  if (trace_path && !trace_dev) CKC(cudaMalloc(&trace_dev, sizeof(unsigned long long) * 4096 * 8));
+  if (trace_path && !trace_dev) CKC(cudaMalloc(&trace_dev, sizeof(unsigned long long) * 4096 * gw::I8_TRACE_SLOTS));
   s.trace = trace_path ? trace_dev : nullptr;
-  if (trace_dev) CKC(cudaMemsetAsync(trace_dev, 0, sizeof(unsigned long long) * 4096 * 8, st));
+  if (trace_dev) CKC(cudaMemsetAsync(trace_dev, 0, sizeof(unsigned long long) * 4096 * gw::I8_TRACE_SLOTS, st));
   static const int dbg_env = getenv("GWAS_I8_DBG") ? atoi(getenv("GWAS_I8_DBG")) : 0;
   s.dbg = dbg_env;
   s.square_a = ft == 0 ? 1 : 0;
@@ -815,7 +815,7 @@ gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, c
   }
   CKC(cudaGetLastError());
   if (trace_dev) {
-    std::vector<unsigned long long> h(4096 * 8);
+    std::vector<unsigned long long> h(4096 * gw::I8_TRACE_SLOTS);
     CKC(cudaStreamSynchronize(st));
     CKC(cudaMemcpy(h.data(), trace_dev, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
     if (FILE* f = fopen(trace_path, "ab")) {
