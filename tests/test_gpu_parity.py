@@ -637,3 +637,27 @@ def test_lowrank_fused_k3_matches_unfused():
         eb, ev = compare(o["b"], o["v"], o["s"], ref, full=True)
         assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
     np.testing.assert_array_equal(outs[0]["s"], outs[1]["s"])
+
+
+# ------------------------------------------------------------------ K3 on the trait-tiled K2 output (t >= 32)
+@pytest.mark.parametrize("n,p,t,m,k,mode,var", [(200, 5, 300, 700, 256, "snp", "literal"),
+                                                (150, 12, 40, 300, 128, "full", "textbook"),
+                                                (120, 1, 129, 333, 200, "full", "literal"),
+                                                (64, 5, 20000, 50, 32, "snp", "textbook")])
+def test_trait_tiled_k3(n, p, t, m, k, mode, var):
+    """Many traits, FP64 exact weights: K2 writes C trait-tiled (ctile.cuh) and K3 streams it with bulk copies
+    (schur_solve_tma): aligned row ranges (t = 40 .. 300) and flattened trait-block ranges (t = 2e4, 157 trait
+    blocks), p = 1 / 5 / 12, SNP and full output, both Var conventions, a monomorphic SNP (status 1, NaN payload),
+    ragged trait blocks (t % 128 != 0) and ragged row tiles -- vs the oracle."""
+    cfg = datagen.custom_config(n=n, p=p, m=m, t=t, index=900 + p + t)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(n)).copy()
+    XR[3, :] = 1                         # SNP 3 monomorphic: collinear with the intercept
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :n].T.astype(np.float64), ds.Y, ds.h2, ds.s2,
+                              var_convention=1 if var == "literal" else 0)
+    assert (ref["status"][3] == oracle.STATUS_COLLINEAR).all()
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), block_cols=k, output_mode=mode, var_convention=var,
+                   overlap=True)
+    eb, ev = compare(b, v, s, ref, full=mode == "full")
+    print(f"tiled K3 n={n} p={p} t={t} {mode}/{var}: max|db|/SE={eb:.2e} Var rel={ev:.2e}")
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
