@@ -204,6 +204,52 @@ class ClockSampler:
                 "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
 
 
+class PcieSampler:
+    """Device PCIe counters while the e2e region runs (NVML nvmlDeviceGetPcieThroughput: bytes over a 20 ms window,
+    polled back to back in a thread): counter evidence for the block staging (H2D = RX, D2H = TX) beside the
+    copy-event timing.  The mean over the windows estimates the average rate of the bursty copies."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rx, self.tx = [], []
+        self._stop = threading.Event()
+        self._th = None
+        self.err = None
+
+    def _loop(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.link = {"gen": pynvml.nvmlDeviceGetCurrPcieLinkGeneration(h),
+                         "width": pynvml.nvmlDeviceGetCurrPcieLinkWidth(h)}
+            while not self._stop.is_set():
+                self.rx.append(pynvml.nvmlDeviceGetPcieThroughput(h, pynvml.NVML_PCIE_UTIL_RX_BYTES))
+                self.tx.append(pynvml.nvmlDeviceGetPcieThroughput(h, pynvml.NVML_PCIE_UTIL_TX_BYTES))
+        except Exception as exc:  # no NVML: report why
+            self.err = repr(exc)
+
+    def __enter__(self):
+        self.link = None
+        self._th = threading.Thread(target=self._loop, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rx:
+            return {"samples": 0, "note": self.err or "no NVML samples"}
+        kb = 1e3 / 1e9  # NVML reports KB/s
+        return {"samples": len(self.rx), "link": self.link,
+                "rx_h2d_gbs_mean": statistics.fmean(self.rx) * kb, "rx_h2d_gbs_max": max(self.rx) * kb,
+                "tx_d2h_gbs_mean": statistics.fmean(self.tx) * kb, "tx_d2h_gbs_max": max(self.tx) * kb,
+                "source": "NVML nvmlDeviceGetPcieThroughput (device PCIe counters, 20 ms windows back to back)"}
+
+
 def fp64_peak():
     """FP64 DMMA peak, BUILDER-measured (MEASURED_PEAKS.json, driver-written, has no FP64 entry):
     tools/fp64_peak.cu, back-to-back mma.sync.m8n8k4.f64 on all SMs (profiles/fp64_peak_r01.json).  It agrees with
@@ -507,11 +553,12 @@ def run_ours(args):
     barrier()
     eng.kernel_times(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        eng.run(xr_host, out=(b_h, v_h, s_h))
-    e1.record(stream)
-    barrier()
+    with PcieSampler(local) as pcie:
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            eng.run(xr_host, out=(b_h, v_h, s_h))
+        e1.record(stream)
+        barrier()
     ms_e2e_rank = e0.elapsed_time(e1)
     ms_e2e = max_over_ranks(ms_e2e_rank, world, dev)
     e2e_value = pairs_total * e2e_steps / (ms_e2e / 1e3)
@@ -655,6 +702,9 @@ def run_ours(args):
                     "h2d_bytes_per_step": sum(p_["info"]["h2d_bytes_per_step"] for p_ in parts),
                     "d2h_bytes_per_step": sum(p_["info"]["d2h_bytes_per_step"] for p_ in parts), "steps": e2e_steps, "ms_per_step": ms_e2e / e2e_steps,
                     "staging_h2d_gbs": staging_gbs,
+                    "pcie_counters": pcie.summary(),
+                    "avg_h2d_gbs": h2d / (ms_e2e_rank / e2e_steps / 1e3) / 1e9,
+                    "avg_d2h_gbs": d2h / (ms_e2e_rank / e2e_steps / 1e3) / 1e9,
                     "staging_note": "pinned host -> HBM block copies on the copy stream (PCIe), timed by CUDA events "
                                     "around each copy while compute runs (rank 0)"},
             "gpu_launches": 3 * len(blocks) * args.steps,
