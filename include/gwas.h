@@ -31,6 +31,7 @@
  *   GWAS_I8_CLUSTER=1|2|4   int8 kernel cluster size (digit-slab multicast), default 2
  *   GWAS_I8_KERNEL=2sm      the 2-SM (cta_group::2) int8 kernel, 8 digits only (measured slower; not the default)
  *   GWAS_BN64_WAVES=w       force the 128/64-wide tile choice of the DMMA kernel by a w-wave threshold
+ *   GWAS_I8_GROUP=g         int8 kernel rasterisation group (row tiles per sweep of the digit slabs), default 32
  *   GWAS_K1_GROUP=g         K1 rasterisation group (row tiles per sweep of the Z panels), default 32
  *   GWAS_K2_GROUP=g         K2 rasterisation group, default 16 (DRAM read per C4 block: 4 -> 10.9, 8 -> 7.9,
  *                           16 -> 6.8, 32 -> 9.8, 64 -> 17.5 GB; time 32.4-32.6 ms for all: DMMA-bound)

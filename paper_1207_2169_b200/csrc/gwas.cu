@@ -772,7 +772,11 @@ gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, c
   s.Cb = Cb;
   s.ldb_c = ldcb;
   s.exps = exps;
-  s.group_m = 64;
+  // rasterisation group (row tiles per sweep of the digit slabs): 32 keeps the group's X_R rows (41 MB at n = 1e4)
+  // L2-resident while the slabs stream; 64 (the whole 8192-SNP block) re-read X_R from DRAM every wave
+  // (C4, 7 digits: DRAM read 10.3 -> 3.3 GB per launch, 7.31 -> 7.04 ms).  GWAS_I8_GROUP overrides (tuning).
+  static const int i8_group = getenv("GWAS_I8_GROUP") ? atoi(getenv("GWAS_I8_GROUP")) : 32;
+  s.group_m = std::max(CL, i8_group);
   s.tri_tiles = (int)tri_tiles;
   if (ft < 0 || ft > gw::I8_FUSE_T) return fail(GWAS_E_ARG, "bad fused-K2b trait count");
   // GWAS_I8_TRACE=<file>: debug phase stamps of the first 4096 CTAs of every launch, appended to <file>
