@@ -690,7 +690,10 @@ gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
   const dim3 grid((unsigned)((a.t + args.tj - 1) / args.tj), (unsigned)((a.cols + snps_per_block - 1) / snps_per_block));
   switch (p) {
 #define CASE_P(P) \
-  case P: gw::schur_solve<P><<<grid, threads, 0, st>>>(args); break;
+  case P:                                                                  \
+    if (args.tiled) gw::schur_solve<P, true><<<grid, threads, 0, st>>>(args); \
+    else gw::schur_solve<P, false><<<grid, threads, 0, st>>>(args);          \
+    break;
     CASE_P(1) CASE_P(2) CASE_P(3) CASE_P(4) CASE_P(5) CASE_P(6)
     CASE_P(7) CASE_P(8) CASE_P(9) CASE_P(10) CASE_P(11) CASE_P(12)
 #undef CASE_P

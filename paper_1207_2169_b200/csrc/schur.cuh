@@ -60,7 +60,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 
 constexpr int SCHUR_ICH = 16;  // SNPs per thread: the trait's factors are loaded once per 16 pairs
 
-template <int P>
+template <int P, bool TILED = false>
 __global__ void __launch_bounds__(128) schur_solve(SchurArgs s) {
   const int j = blockIdx.x * s.tj + (int)(threadIdx.x % (unsigned)s.tj);
   const int ii = (int)(threadIdx.x / (unsigned)s.tj);
@@ -82,11 +82,11 @@ __global__ void __launch_bounds__(128) schur_solve(SchurArgs s) {
   // the kernel is HBM-bound, each thread walks its SNP chunk sequentially)
   // field f of pair (i, j) is at C[i * ldc + jo + f * fs] (f < P; the y field too when tiled), r_ij at
   // Cy[i * ldcy + jy], c_ij at C[i * ldc + sqo]
-  const long long jo = s.tiled ? ctile_off(j, 0, P + 2) : j;
-  const long long fs = s.tiled ? CTILE_T : t;
-  const double* Cy = s.tiled ? s.C + jo + (long long)P * CTILE_T : s.Cy + j;
-  const long long ldcy = s.tiled ? s.ldc : s.ldcy;
-  const long long sqo = s.tiled ? jo + (long long)(P + 1) * CTILE_T : (long long)s.nsq + j;
+  const long long jo = TILED ? ctile_off(j, 0, P + 2) : j;
+  const long long fs = TILED ? CTILE_T : t;
+  const double* Cy = TILED ? s.C + jo + (long long)P * CTILE_T : s.Cy + j;
+  const long long ldcy = TILED ? s.ldc : s.ldcy;
+  const long long sqo = TILED ? jo + (long long)(P + 1) * CTILE_T : (long long)s.nsq + j;
   double nxt[P + 2];
   auto load = [&](int i, double (&x)[P + 2]) {
     const double* row = s.C + (long long)i * s.ldc + jo;
