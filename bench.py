@@ -307,6 +307,13 @@ def cpu_model():
 
 
 # ------------------------------------------------------------------ oracle (cpu_baseline / --impl reference)
+def all_host_cores():
+    """The oracle runs on all of the host's cores: torch.distributed.run sets OMP_NUM_THREADS=1 in every rank, which
+    would otherwise leave rank 0's LAPACK (parity check, cpu_baseline, the reference arm) on one thread."""
+    import threadpoolctl
+    return threadpoolctl.threadpool_limits(limits=host_cores())
+
+
 def _blas_threads():
     import threadpoolctl
     info = threadpoolctl.threadpool_info()
@@ -667,7 +674,8 @@ def run_ours(args):
     else:
         parts = [payload]
     if args.check and rank == 0:
-        parity = check_parity(gcfg, ds, sub, parts)
+        with all_host_cores():
+            parity = check_parity(gcfg, ds, sub, parts)
         for name, pr in list(parity["modes"].items()):
             if name in modes:
                 modes[name]["parity"] = pr
@@ -717,7 +725,8 @@ def run_ours(args):
         if parity is not None:
             res["parity"] = {k: v for k, v in parity.items() if k != "modes"}
         if not args.no_cpu_baseline:
-            res["cpu_baseline"] = cpu_baseline(cfg, ds, args)
+            with all_host_cores():
+                res["cpu_baseline"] = cpu_baseline(cfg, ds, args)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -811,7 +820,8 @@ def run_reference(args):
     for step in range(args.warmup + args.steps):
         traits = np.array([int(rng.integers(cfg.t))])
         snps = np.sort(rng.choice(cfg.m, size=min(cfg.m, args.ref_snps), replace=False))
-        pairs, sec, thr = oracle_sample(cfg, ds, traits, snps)
+        with all_host_cores():
+            pairs, sec, thr = oracle_sample(cfg, ds, traits, snps)
         if step >= args.warmup:
             times.append(sec)
             pairs_all += pairs
