@@ -661,3 +661,29 @@ def test_trait_tiled_k3(n, p, t, m, k, mode, var):
     eb, ev = compare(b, v, s, ref, full=mode == "full")
     print(f"tiled K3 n={n} p={p} t={t} {mode}/{var}: max|db|/SE={eb:.2e} Var rel={ev:.2e}")
     assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+# ------------------------------------------------------------------ block_cols = 0 (auto)
+@pytest.mark.parametrize("n,p,t,m", [(17, 2, 1, 40), (333, 3, 37, 777), (200, 4, 4, 2000), (1000, 4, 1000, 300)])
+def test_auto_block_size(n, p, t, m):
+    """block_cols = 0: the library picks k (a multiple of 128 in [4096, 16384], reported by gwas_run_info) from the
+    wave quantisation of K1/K2; results are bitwise those of a fixed k and match the oracle."""
+    gw = _gw()
+    cfg = datagen.custom_config(n=n, p=p, m=m, t=t, index=950 + n + t)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(n))
+    dev = torch.from_numpy(XR).cuda()
+    eng = gw.Gwas(n, p, t, device=0, block_cols=0, overlap=True)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    info = eng.run_info()
+    assert 4096 <= info["block_cols"] <= 16384 and info["block_cols"] % 128 == 0
+    b, v, s = eng.run(dev)
+    torch.cuda.synchronize()
+    auto = (b.cpu().numpy(), v.cpu().numpy(), s.cpu().numpy())
+    eng.close()
+    fixed = _run(cfg, ds, dev, block_cols=96)
+    for x, y in zip(auto, fixed):
+        np.testing.assert_array_equal(x, y)
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    eb, ev = compare(*auto, ref)
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
