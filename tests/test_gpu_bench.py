@@ -78,3 +78,22 @@ def test_bench_two_ranks_gloo_on_one_gpu():
     assert d["setup"]["broadcast_bytes"] > 0 and d["parity"]["pass"]
     assert d["modes"]["int8_sliced"]["parity"]["pass"]
     assert [r["rank"] for r in d["parity"]["per_rank"]] == [0, 1]   # rank 1's shard is checked too
+
+
+def test_bench_nccl_ranks_when_gpus_available():
+    """With >= 2 visible GPUs: `bench.py --gpus 2` (self-launch, NCCL, one GPU per rank) on config 0 -- two distinct
+    GPU UUIDs, NCCL INIT lines naming 2 ranks, the state broadcast timed, and a passing parity check on both shards.
+    Skipped on a one-GPU box (this pool), where test_bench_self_launches_n_ranks covers the path over gloo."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "GWAS_BENCH_BACKEND")}
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "0", "--steps", "1", "--warmup", "3",
+                          "--no-cpu-baseline", "--no-est-alt"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["n_gpus"] == 2 and len({r["gpu_uuid"] for r in d["ranks"]}) == 2
+    assert any("nRanks 2" in ln for r in d["ranks"] for ln in r["nccl_init"])
+    assert d["setup"]["ms_broadcast"] > 0 and d["parity"]["pass"]
+    assert [r["rank"] for r in d["parity"]["per_rank"]] == [0, 1]
