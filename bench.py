@@ -156,14 +156,27 @@ def blocks_of(ncols: int, block: int):
     return [min(block, ncols - c) for c in range(0, ncols, block)]
 
 
+def nvml_id(device) -> str:
+    """The nvidia-smi / NVML identifier of a torch CUDA device: its UUID ("GPU-..."), because CUDA's device order
+    (and CUDA_VISIBLE_DEVICES) need not match NVML's PCI order on a multi-GPU node; the CUDA ordinal as a fallback."""
+    try:
+        import torch
+        u = str(torch.cuda.get_device_properties(device).uuid)
+        if u:
+            return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        pass
+    return str(device.index if hasattr(device, "index") else device)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs."""
     FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
              "clocks_event_reasons.sw_power_cap"
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index):
+        self.index = index  # nvml_id(): UUID or ordinal
         self.rows = []
         self._stop = threading.Event()
         self._th = None
@@ -209,8 +222,8 @@ class PcieSampler:
     polled back to back in a thread): counter evidence for the block staging (H2D = RX, D2H = TX) beside the
     copy-event timing.  The mean over the windows estimates the average rate of the bursty copies."""
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index):
+        self.index = index  # nvml_id(): UUID or ordinal
         self.rx, self.tx = [], []
         self._stop = threading.Event()
         self._th = None
@@ -220,7 +233,8 @@ class PcieSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            h = (pynvml.nvmlDeviceGetHandleByUUID(self.index) if str(self.index).startswith("GPU-")
+                 else pynvml.nvmlDeviceGetHandleByIndex(int(self.index)))
             self.link = {"gen": pynvml.nvmlDeviceGetCurrPcieLinkGeneration(h),
                          "width": pynvml.nvmlDeviceGetCurrPcieLinkWidth(h)}
             while not self._stop.is_set():
@@ -513,7 +527,7 @@ def run_ours(args):
     stream = eng.compute_stream
     for _ in range(args.warmup):
         eng.run(xr_dev, out=out)
-    with ClockSampler(local) as clk:
+    with ClockSampler(nvml_id(dev)) as clk:
         ms = _timed_steps(eng, xr_dev, out, args.steps, stream, barrier)
     ms_max = max_over_ranks(ms, world, dev)
     pairs_total = float(m_total) * t
@@ -560,7 +574,7 @@ def run_ours(args):
     barrier()
     eng.kernel_times(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with PcieSampler(local) as pcie:
+    with PcieSampler(nvml_id(dev)) as pcie:
         e0.record(stream)
         for _ in range(e2e_steps):
             eng.run(xr_host, out=(b_h, v_h, s_h))

@@ -45,7 +45,7 @@ def main():
         o = (out[0][lo:hi], out[1][lo:hi], out[2][lo:hi])
         for _ in range(a.warmup):
             eng.run(xr[lo:hi], out=o)
-        with bench.ClockSampler(0) as clk:
+        with bench.ClockSampler(bench.nvml_id(dev)) as clk:
             ms = bench._timed_steps(eng, xr[lo:hi], o, a.steps, eng.compute_stream, torch.cuda.synchronize)
         t_shard = ms / a.steps
         rows.append({"n_gpus": n_gpus, "shard_snps": hi - lo, "ms_per_step_shard": t_shard,
