@@ -1,7 +1,9 @@
 """cuBLAS DGEMM yardstick (torch.matmul fp64) on the K1/K2 shapes of SURVEY.md §8(d). Not product code."""
 import json, torch
 dev = torch.device("cuda:0")
-for (M, N, K, name) in [(8192, 10000, 10000, "K1_C4"), (8192, 7000, 10000, "K2_C4"), (8192, 1000, 1000, "K1_C1"), (8192, 6000, 1000, "K2_C2"), (8192, 8192, 8192, "sq8192")]:
+for (M, N, K, name) in [(8192, 10000, 10000, "K1_C4"), (8192, 7000, 10000, "K2_C4"), (15104, 10000, 10000, "K1_C4_k15104"),
+                        (15104, 7016, 10000, "K2_C4_k15104"), (8192, 1000, 1000, "K1_C1"), (8192, 6000, 1000, "K2_C2"),
+                        (4736, 7016, 1000, "K2_C2_k4736"), (8192, 8192, 8192, "sq8192")]:
     a = torch.randn(M, K, dtype=torch.float64, device=dev)
     b = torch.randn(K, N, dtype=torch.float64, device=dev)
     for _ in range(3):
