@@ -219,6 +219,14 @@ def test_setup_errors():
         b, v, s = eng.alloc_outputs(4)
         L.check(L.lib.gwas_run(eng._ctx, 4, XR.ctypes.data, 64, b.data_ptr(), v.data_ptr(), s.data_ptr()))
     assert e.value.code == 1
+    # the round-2 queries: run configuration, and estimation diagnostics only on an estimation context
+    import ctypes as C
+    import paper_1207_2169_b200._lib as L
+    info = eng.run_info()
+    assert info["block_cols"] == 8192 and info["fused_k2"] is True   # t (p + 2) = 10 <= 28: K2 in K1's epilogue
+    gs = np.zeros(cfg.t, dtype=np.int32)
+    assert L.lib.gwas_estimate_grid_argmax(eng._ctx, gs.ctypes.data_as(C.POINTER(C.c_int32))) == L.GWAS_E_STATE
+    assert L.lib.gwas_run_info(None, None, None) == L.GWAS_E_STATE
     eng.close()
 
 
