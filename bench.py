@@ -625,6 +625,62 @@ def run_ours(args):
         eng8.close()
         ser8.close()
 
+    # ================= fp64 X_R staged from pinned host (the PCIe roofline; SURVEY §8(d) staging check) ==========
+    # uint8 dosages are the default (1 byte per entry); with fp64 dosages (8 bytes) the small-n configs become
+    # staging-bound: n = 1e3, t = 1 needs 8 KB per SNP over PCIe against 2n^2 = 2e6 flop of K1.  Only where the fp64
+    # shard fits a modest pinned buffer (<= 8 GB).
+    if args.f64_alt and ncols * ld * 8 <= 8e9:
+        x64_h = torch.empty((ncols, ld), dtype=torch.float64, pin_memory=True)
+        x64_h.copy_(xr_host)
+        # the PCIe yardstick: plain pinned -> HBM copies of the same bytes in the same 8192-SNP pieces, back to back
+        # on one stream (no compute), best of two passes
+        probe = torch.empty((min(ncols, 8192), ld), dtype=torch.float64, device=dev)
+        pcie_gbs = 0.0
+        for _ in range(2):
+            ep0, ep1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            ep0.record()
+            for c0 in range(0, ncols, 8192):
+                c1 = min(ncols, c0 + 8192)
+                probe[: c1 - c0].copy_(x64_h[c0:c1], non_blocking=True)
+            ep1.record()
+            torch.cuda.synchronize(dev)
+            pcie_gbs = max(pcie_gbs, ncols * ld * 8 / (ep0.elapsed_time(ep1) / 1e3) / 1e9)
+        del probe
+        eng64 = gw.Gwas(n, p, t, device=local, block_cols=args.block, timing=True, overlap=True, xr_dtype="f64",
+                        fuse_k2=bool(args.fuse_k2))
+        if rank == 0:
+            eng64.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+        if world > 1:
+            barrier()
+            replicate_state(eng64.state, world)
+            barrier()
+            if rank != 0:
+                eng64.attach()
+        for _ in range(args.warmup):
+            eng64.run(x64_h, out=out)
+        eng64.kernel_times(reset=True)
+        ms64 = max_over_ranks(_timed_steps(eng64, x64_h, out, args.steps, eng64.compute_stream, barrier), world, dev)
+        kt64 = eng64.kernel_times(reset=True)
+        cut("fp64_staged", out)
+        h2d64 = ncols * ld * 8
+        modes["fp64_staged"] = {
+            "value": pairs_total * args.steps / (ms64 / 1e3), "unit": UNIT, "ms_per_step": ms64 / args.steps,
+            "what": "X_R as fp64 dosages in pinned host memory, staged block by block on the copy stream (device "
+                    "outputs), K1/K2 on FP64 DMMA",
+            "roofline": {"bound": "pcie" if h2d64 / (ms64 / args.steps / 1e3) / 1e9 >= 0.8 * pcie_gbs
+                         else "compute (staging hidden behind K1/K2)",
+                         "achieved": h2d64 * world / (ms64 / args.steps / 1e3) / 1e9,
+                         "peak": pcie_gbs, "unit": "GB/s",
+                         "frac": h2d64 / (ms64 / args.steps / 1e3) / 1e9 / pcie_gbs,
+                         "peak_source": "measured in this run: plain pinned-host -> HBM copies of the same bytes "
+                                        "in 8192-SNP pieces, back to back, no compute"},
+            "staging_h2d_gbs_events": h2d64 * args.steps / (kt64["H2D"]["ms"] / 1e3) / 1e9
+            if kt64["H2D"]["ms"] > 0 else None,
+            "h2d_bytes_per_step": h2d64 * world}
+        eng64.close()
+        del x64_h
+
     # ================= CLAK-Chol single-trait path (Alg. 3, NEXT-1), t == 1 only =================
     if t == 1 and args.chol_alt:
         for i8 in (0, args.int8_slices):
@@ -902,6 +958,8 @@ def build_parser():
                     help="skip the int8-sliced mode measurement reported under `modes`")
     ap.add_argument("--lowrank-alt", dest="lowrank_alt", action="store_true",
                     help="also time the low-rank trait-weight modes (reading L1, outside SURVEY §8) for t >= 16")
+    ap.add_argument("--no-f64-alt", dest="f64_alt", action="store_false",
+                    help="skip the fp64-dosage staged run (`modes.fp64_staged`, PCIe roofline; shards <= 8 GB in fp64)")
     ap.add_argument("--no-est-alt", dest="est_alt", action="store_false",
                     help="skip the variance-component estimation measurement reported under `modes.estimate`")
     ap.add_argument("--e2e-steps", type=int, default=2)
