@@ -210,6 +210,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, BN == 64 ? 2 : 1)
     const int r = pid - g * per_group;
     tm = first_m + r % gsz;
     tn = r / gsz;
+    // lower-triangular B (CLAK-Chol): tile tn needs (tn + 1) k-panels; run the long tiles first so the short ones
+    // fill the last wave (longest-processing-time order)
+    if (s.tri) tn = s.tiles_n - 1 - tn;
   }
   const int m0 = tm * BM, n0 = tn * BN;
   const int kt_begin = split * s.kt_per_split;
