@@ -76,3 +76,30 @@ def test_full_config_subsample_chol(index, i8):
     eb, ev = compare(bs, vs, ss, ref)
     print(f"C{index} chol int8_slices={i8}: {snps.size} pairs, max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
     assert eb <= TOL_B and ev <= TOL_VAR
+
+
+def test_full_config_c1_fp64_dosages_staged_from_host():
+    """C1 at full size with X_R as fp64 dosages in pinned HOST memory (staged block by block on the copy stream,
+    results streamed back to pinned host memory) -- the bench's `modes.fp64_staged` path -- vs the oracle."""
+    import paper_1207_2169_b200 as gw
+    cfg = datagen.CONFIGS[1]
+    ds = datagen.dataset(cfg, device=torch.device("cuda", 0))
+    ld = (cfg.n + 1) // 2 * 2                       # 16-byte rows for fp64
+    xr8 = torch.empty((cfg.m, ld), dtype=torch.uint8)
+    datagen.xr_dosages(cfg, ld=ld, out=xr8.numpy())
+    x64 = torch.empty((cfg.m, ld), dtype=torch.float64, pin_memory=True)
+    x64.copy_(xr8)
+    eng = gw.Gwas(cfg.n, cfg.p, cfg.t, device=0, block_cols=0, xr_dtype="f64", overlap=True)
+    eng.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2)
+    b, v, s = eng.alloc_outputs(cfg.m, host=True)
+    eng.run(x64, out=(b, v, s))
+    torch.cuda.synchronize()
+    k = eng.run_info()["block_cols"]
+    eng.close()
+    snps, traits = datagen.subsample(cfg, forced_snps=[k - 1, k, (cfg.m - 1) // k * k])
+    G = datagen.xr_columns(cfg, snps)
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, G, ds.Y, ds.h2, ds.s2, traits=traits)
+    bs, vs, ss = (x.numpy()[np.ix_(snps, traits)] for x in (b, v, s))
+    eb, ev = compare(bs, vs, ss, ref)
+    print(f"C1 fp64 dosages from host: {snps.size * traits.size} pairs, max|db|/SE={eb:.3e}, max Var rel={ev:.3e}")
+    assert eb <= TOL_B and ev <= TOL_VAR

@@ -155,3 +155,16 @@ def test_work_model():
     assert f["K1"] == 2 * 10_000 ** 2 * 8192
     assert f["K2"] == 2 * 10_000 * 8192 * 1000 * 7
     assert bench.k3_bytes(5, 1000, 8192) == 8192 * 1000 * (8 * 7 + 17)
+
+
+def test_parity_edges_weak_scaling():
+    """Weak scaling (opt-in): rank r owns [r m, (r+1) m) of an N m genome; its edges and block edges are forced."""
+    m, world, k = 50_000, 4, 8192
+    edges = bench.parity_edges(m, world, "weak", k)
+    for r in range(world):
+        lo, hi = bench.shard_range(m, r, world, "weak")
+        assert (lo, hi) == (r * m, (r + 1) * m)
+        assert lo in edges and hi - 1 in edges and lo + k in edges
+    cfg = datagen.custom_config(n=32, p=2, m=m * world, t=3, index=77)
+    snps, traits = bench.parity_subsample(cfg, m, world, "weak", k, 1_000)
+    assert snps.max() < m * world and set(edges) <= set(snps.tolist())
