@@ -29,6 +29,7 @@ gives every rank its own m SNPs of an N m-SNP genome.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import socket
@@ -170,13 +171,15 @@ def nvml_id(device) -> str:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs."""
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs, for one GPU or -- on rank 0
+    of a multi-GPU run -- every rank's GPU in one query (`index`: an nvml_id or a list of them)."""
     FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-             "clocks_event_reasons.sw_power_cap"
+             "clocks_event_reasons.sw_power_cap,uuid"
 
     def __init__(self, index):
-        self.index = index  # nvml_id(): UUID or ordinal
+        ids = [str(x) for x in index] if isinstance(index, (list, tuple)) else [str(index)]
+        self.ids = list(dict.fromkeys(ids))  # ranks sharing a GPU (gloo test mode) query it once
         self.rows = []
         self._stop = threading.Event()
         self._th = None
@@ -184,11 +187,12 @@ class ClockSampler:
     def _loop(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                out = subprocess.run(["nvidia-smi", "-i", ",".join(self.ids), f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                vals = [v.strip() for v in out.strip().split(",")]
-                if len(vals) >= 8:
-                    self.rows.append(vals)
+                for ln in out.strip().splitlines():
+                    vals = [v.strip() for v in ln.split(",")]
+                    if len(vals) >= 9:
+                        self.rows.append(vals)
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -203,18 +207,35 @@ class ClockSampler:
         if self._th:
             self._th.join(timeout=10)
 
+    @staticmethod
+    def _num(x):
+        try:
+            return float(x)
+        except ValueError:
+            return None
+
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
-        counts = {names[i]: sum(1 for r in self.rows if r[4 + i].lower().startswith("active")) for i in range(4)}
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "reason_samples": {k: v for k, v in counts.items() if v},
-                "samples": len(self.rows),
-                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
+
+        def summ(rows):
+            sm = [v for v in (self._num(r[0]) for r in rows) if v is not None]
+            smax = [v for v in (self._num(r[1]) for r in rows) if v is not None]
+            pw = [v for v in (self._num(r[2]) for r in rows) if v is not None]
+            counts = {names[i]: sum(1 for r in rows if r[4 + i].lower().startswith("active")) for i in range(4)}
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                    "reasons": sorted(k for k, v in counts.items() if v),
+                    "reason_samples": {k: v for k, v in counts.items() if v}, "samples": len(rows),
+                    "power_w_max": max(pw) if pw else None}
+
+        out = summ(self.rows)
+        gpus = sorted({r[8] for r in self.rows})
+        if len(gpus) > 1:  # multi-GPU: the slowest GPU's median and each GPU's own summary
+            per = {g: summ([r for r in self.rows if r[8] == g]) for g in gpus}
+            out["sm_mhz"] = min(v["sm_mhz"] for v in per.values() if v["sm_mhz"] is not None)
+            out["per_gpu"] = per
+        return out
 
 
 class PcieSampler:
@@ -527,7 +548,12 @@ def run_ours(args):
     stream = eng.compute_stream
     for _ in range(args.warmup):
         eng.run(xr_dev, out=out)
-    with ClockSampler(nvml_id(dev)) as clk:
+    if world > 1:  # rank 0 samples every rank's GPU in one nvidia-smi query (one sampler per node, not per rank)
+        ids = [None] * world
+        dist.all_gather_object(ids, nvml_id(dev))
+    else:
+        ids = [nvml_id(dev)]
+    with (ClockSampler(ids) if rank == 0 else contextlib.nullcontext()) as clk:
         ms = _timed_steps(eng, xr_dev, out, args.steps, stream, barrier)
     ms_max = max_over_ranks(ms, world, dev)
     pairs_total = float(m_total) * t
@@ -574,7 +600,7 @@ def run_ours(args):
     barrier()
     eng.kernel_times(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with PcieSampler(nvml_id(dev)) as pcie:
+    with (PcieSampler(nvml_id(dev)) if rank == 0 else contextlib.nullcontext()) as pcie:
         e0.record(stream)
         for _ in range(e2e_steps):
             eng.run(xr_host, out=(b_h, v_h, s_h))
