@@ -695,3 +695,20 @@ def test_auto_block_size(n, p, t, m):
     ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
     eb, ev = compare(*auto, ref)
     assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
+
+
+@pytest.mark.parametrize("i8", [0, 8])
+def test_minimum_n_square_design(i8):
+    """n = w = p + 1 (the smallest n the problem admits): every X_i is square, the GLS solution interpolates,
+    b = X_i^-1 y_j and Var = X_i^-1 M_j X_i^-T (pin P8 of the oracle) -- through every kernel at its smallest shape."""
+    p = 4
+    n = p + 1
+    cfg = datagen.custom_config(n=n, p=p, m=64, t=3, S=64, index=990)
+    ds = datagen.dataset(cfg)
+    XR = datagen.xr_dosages(cfg, ld=_ld(n))
+    ref = oracle.gls_sequence(ds.Phi, ds.XL, XR[:, :n].T.astype(np.float64), ds.Y, ds.h2, ds.s2)
+    b, v, s = _run(cfg, ds, torch.from_numpy(XR).cuda(), int8_slices=i8, block_cols=16)
+    np.testing.assert_array_equal(s, ref["status"])
+    eb, ev = compare(b, v, s, ref)
+    # square systems amplify rounding by cond(X_i); the tolerance stays the north star's
+    assert eb <= TOL_B and ev <= TOL_VAR, (eb, ev)
