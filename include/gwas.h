@@ -33,10 +33,12 @@
  *   GWAS_BN64_WAVES=w       force the 128/64-wide tile choice of the DMMA kernel by a w-wave threshold
  *   GWAS_I8_GROUP=g         int8 kernel rasterisation group (row tiles per sweep of the digit slabs), default 32
  *   GWAS_K1_GROUP=g         K1 rasterisation group (row tiles per sweep of the Z panels), default 32
- *   GWAS_K2_GROUP=g         K2 rasterisation group, default 16 (DRAM read per C4 block: 4 -> 10.9, 8 -> 7.9,
- *                           16 -> 6.8, 32 -> 9.8, 64 -> 17.5 GB; time 32.4-32.6 ms for all: DMMA-bound)
- *   GWAS_I8_TRACE=<file>    append %globaltimer phase stamps of the int8 kernel to <file> (allocates a 256 KB
- *                           device buffer and synchronises after every launch)
+ *   GWAS_K2_GROUP=g         K2 rasterisation group, default 16 (DRAM read per 8192-SNP C4 block: 4 -> 10.9,
+ *                           8 -> 7.9, 16 -> 6.8, 32 -> 9.8, 64 -> 17.5 GB; per 15104-SNP block 8 / 16 / 32 -> 19.3 /
+ *                           15.5 / 22.5 GB; time unchanged: DMMA-bound)
+ *   GWAS_I8_TRACE=<file>    append the int8 kernel's debug trace to <file>: per CTA 16 slots -- %globaltimer phase
+ *                           stamps, SM id, clock64 cycles waited on full / empty barriers, k-stages (tools/i8_trace.py;
+ *                           allocates a 512 KB device buffer and synchronises after every launch)
  *   GWAS_I8_DBG=1|2         int8 epilogue without TMEM loads / stores (timing experiments; results invalid)
  *   GWAS_K3_PLAIN=1         K3 on the trait-tiled C with the register-prefetch kernel instead of the bulk-copy
  *                           (TMA) streamed one (comparison only; bitwise identical results)
