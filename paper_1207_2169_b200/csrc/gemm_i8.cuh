@@ -29,24 +29,37 @@
 
 namespace gw {
 
-constexpr int I8_SLICES = 8;       // digits per fp64 value of the exact variant (the 2-SM kernel supports only this)
+constexpr int I8_SLICES = 8;       // digits per fp64 value of the exact variant
 constexpr int I8_NB = 64;          // output columns per tile
 constexpr int I8_BM = 128;         // output rows (SNPs) per tile
-constexpr int I8_BKB = 64;         // K bytes per stage (64-byte swizzle atom rows)
-constexpr int I8_STAGES = 5;
 constexpr int I8_THREADS = 256;
-constexpr int I8_BROWS = I8_SLICES * I8_NB;  // 512 B rows per tile = TMEM columns
+constexpr size_t I8_SMEM_MAX = 232448;  // 227 KB opt-in shared memory per CTA
 
+// K bytes per pipeline stage, BKB = 64 (64-byte swizzle atoms, the round-1/2 layout) or 128 (128-byte swizzle: each
+// TMA box row is one 128-byte request instead of two 64-byte ones, half the TMA row requests per byte).
 // Per digit count S (int8_slices = 7 or 8): B rows per tile (S x 64, TMEM columns of the accumulators) and the
-// stage ring depth that fits 227 KB of shared memory (A 8 KB + B S x 4 KB per 64-byte K stage).
-template <int S>
+// stage ring depth that fits 227 KB of shared memory (A 128 x BKB + B S x 64 x BKB bytes per stage).
+template <int S, int BKB>
 struct I8Cfg {
   static_assert(S == 7 || S == 8, "int8_slices must be 7 or 8");
+  static_assert(BKB == 64 || BKB == 128, "K stage of 64 or 128 bytes");
   static constexpr int BROWS = S * I8_NB;
-  static constexpr int STAGES = S == 8 ? 5 : 6;
-  static constexpr size_t smem_bytes(size_t epi) {
-    return 1024 + (size_t)STAGES * (I8_BM + BROWS) * I8_BKB + 256 + epi;
-  }
+  static constexpr size_t fixed = 1024 + 256;  // alignment slack + barriers
+  static constexpr int STAGES = (int)((I8_SMEM_MAX - fixed - 4608) / ((size_t)(I8_BM + BROWS) * BKB));
+  static_assert(STAGES >= 2 && STAGES <= 15, "ring depth");
+  static constexpr size_t smem_bytes(size_t epi) { return fixed + (size_t)STAGES * (I8_BM + BROWS) * BKB + epi; }
+};
+// 2-SM kernel: per CTA a stage holds its 128 A rows and half of each N chunk of the slab (chunk 0 = digits 0..3,
+// 256 rows -> 128 per CTA; chunk 1 = digits 4..S-1, (S - 4) x 64 rows -> (S - 4) x 32 per CTA).
+template <int S, int BKB>
+struct I8Cfg2 {
+  static_assert(S == 7 || S == 8, "int8_slices must be 7 or 8");
+  static constexpr int NC1 = (S - 4) * 32;  // chunk-1 rows per CTA
+  static constexpr int BH_ROWS = 128 + NC1;
+  static constexpr size_t fixed = 1024 + 256;
+  static constexpr int STAGES = (int)((I8_SMEM_MAX - fixed - 4608) / ((size_t)(I8_BM + BH_ROWS) * BKB));
+  static_assert(STAGES >= 2 && STAGES <= 15, "ring depth");
+  static constexpr size_t smem_bytes(size_t epi) { return fixed + (size_t)STAGES * (I8_BM + BH_ROWS) * BKB + epi; }
 };
 
 struct I8Shape {
@@ -76,17 +89,21 @@ struct I8Shape {
 };
 constexpr int I8_FUSE_T = 8;
 
-__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
-  // K-major, 64-byte swizzle: 8-row atoms of 64 B (SBO = 512 B between atoms), LBO unused (encoded 1),
-  // version 1 (sm_100), base offset 0 (tiles are 1024-byte aligned), layout type 4 = SWIZZLE_64B.
+template <int BKB>
+__device__ __forceinline__ uint64_t umma_desc_k(uint32_t smem_addr) {
+  // K-major, BKB-byte swizzle: 8-row atoms of BKB bytes (SBO = 8 x BKB between atoms), LBO unused (encoded 1),
+  // version 1 (sm_100), base offset 0 (tiles are 1024-byte aligned), layout type 4 = SWIZZLE_64B, 2 = SWIZZLE_128B.
+  // A K step of 32 bytes inside the atom advances the start address (the swizzle acts on absolute address bits).
+  static_assert(BKB == 64 || BKB == 128, "swizzle width");
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)(((8 * BKB) >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;
+  d |= (uint64_t)(BKB == 128 ? 2 : 4) << 61;
   return d;
 }
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) { return umma_desc_k<64>(smem_addr); }
 
 // kind::i8 instruction descriptor: D s32, A u8, B s8, both K-major, M = 128, N = n.
 __host__ __device__ constexpr uint32_t idesc_i8(int n) {
@@ -278,13 +295,14 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
 // column tile, and each loads 1/CL of the shared digit slab and multicasts it to all (L2 reads of the dominant
 // B operand / CL).  Stage slots are released cluster-wide: every CTA's MMA completion arrives on every CTA's
 // empty barrier (count CL).
-template <int CL, int S>
+template <int CL, int S, int BKB>
 __global__ void __launch_bounds__(I8_THREADS, 1)
     gemm_i8_sliced(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Shape s) {
-  constexpr int I8_STAGES = I8Cfg<S>::STAGES;
-  constexpr int BROWS = I8Cfg<S>::BROWS;       // S x 64
-  constexpr int A_BYTES = I8_BM * I8_BKB;      // 8 KB
-  constexpr int B_BYTES = BROWS * I8_BKB;      // S x 4 KB
+  constexpr int I8_STAGES = I8Cfg<S, BKB>::STAGES;
+  constexpr int I8_BKB = BKB;
+  constexpr int BROWS = I8Cfg<S, BKB>::BROWS;  // S x 64
+  constexpr int A_BYTES = I8_BM * I8_BKB;      // 8 or 16 KB
+  constexpr int B_BYTES = BROWS * I8_BKB;      // S x 4 or 8 KB
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -378,9 +396,9 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         const uint32_t b0 = smem_u32(sB + st * B_BYTES);
 #pragma unroll
         for (int kk = 0; kk < I8_BKB / 32; ++kk) {
-          const uint64_t ad = umma_desc_sw64(a0 + kk * 32);
-          const uint64_t bd0 = umma_desc_sw64(b0 + kk * 32);
-          const uint64_t bd1 = umma_desc_sw64(b0 + 256 * I8_BKB + kk * 32);
+          const uint64_t ad = umma_desc_k<BKB>(a0 + kk * 32);
+          const uint64_t bd0 = umma_desc_k<BKB>(b0 + kk * 32);
+          const uint64_t bd1 = umma_desc_k<BKB>(b0 + 256 * I8_BKB + kk * 32);
           const uint32_t acc = (kb | kk) ? 1u : 0u;
           umma_i8(tmem_base, ad, bd0, idesc, acc);
           umma_i8(tmem_base + 256, ad, bd1, idesc2, acc);
@@ -410,14 +428,13 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
 
 // ---------------------------------------------------------------------------------------------------------------
 // 2-SM variant (tcgen05 cta_group::2): a CTA pair computes a 256 x 64 output tile with M = 256 MMAs issued by the
-// pair's leader CTA.  Each CTA stages its own 128 A rows and HALF of the 512-row digit slab (for each N = 256
-// chunk c, rows c*256 + rank*128 .. +127); the tensor cores of both SMs read both halves, so every slab byte is
-// fetched and written to shared memory once per pair (vs once per CTA), which relieves the shared-memory
-// bandwidth that bounds the 1-SM kernel (TMA writes + UMMA reads).  Each CTA's TMEM holds its own 128 rows x
-// 512 accumulator columns, drained by its own epilogue warps.  TMA loads of both CTAs signal the leader's full
+// pair's leader CTA.  Each CTA stages its own 128 A rows and HALF of each N chunk of the S x 64-row digit slab
+// (chunk 0 = digits 0..3: rows rank*128 .. +127; chunk 1 = digits 4..S-1: rows 256 + rank*(S-4)*32 ..); the tensor
+// cores of both SMs read both halves, so every slab byte is fetched and written to shared memory once per pair (vs
+// once per CTA): per SM (128 + S x 32) x K bytes land per 2 x 128 x S x 64 x K ops instead of (128 + S x 64) x K,
+// which relieves the TMA / crossbar bandwidth that bounds the 1-SM kernel.  Each CTA's TMEM holds its own 128 rows x
+// S x 64 accumulator columns, drained by its own epilogue warps.  TMA loads of both CTAs signal the leader's full
 // barrier; the leader's commits arrive on both CTAs' empty / tmem_full barriers.
-constexpr int I8_STAGES2 = 8;
-
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   // the mbarrier operand addresses the LEADER CTA's barrier (peer bit cleared), as for 2-SM UMMA pipelines
   const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
@@ -425,6 +442,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_leader)
+      : "memory");
+}
+
+// The same with the slab multicast to the same-role CTA of every pair in the cluster (each destination CTA's bytes
+// complete_tx on ITS pair leader's barrier: the peer bit of the barrier address is cleared).
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                   uint16_t mask) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_leader), "h"(mask)
       : "memory");
 }
 
@@ -436,11 +465,11 @@ __device__ __forceinline__ void umma_i8_2sm(uint32_t tmem_d, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar) {
+__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
           smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(mask)
       : "memory");
 }
 
@@ -448,46 +477,60 @@ __host__ __device__ constexpr uint32_t idesc_i8_m256(int n) {
   return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
+// CLP pairs per cluster (1 or 2): with 2, the two pairs compute consecutive 256-row tiles of the same column tile and
+// share its digit slab: the CTA of role r in pair q fetches the q-th 1/CLP of its slab half and multicasts it to role r
+// of every pair (L2 reads of the slab / CLP); stage slots are then released cluster-wide (empty count CLP, every
+// leader's commit multicast to all CTAs).  tmB: box of 128 / CLP slab rows (chunk 0); tmB1: box of (S - 4) x 32 / CLP
+// rows (chunk 1).
+template <int S, int BKB, int CLP>
 __global__ void __launch_bounds__(I8_THREADS, 1)
-    gemm_i8_sliced_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Shape s) {
-  constexpr int A_BYTES = I8_BM * I8_BKB;              // 8 KB: this CTA's 128 rows
-  constexpr int BH_BYTES = (I8_BROWS / 2) * I8_BKB;    // 16 KB: this CTA's half of the slab
+    gemm_i8_sliced_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ CUtensorMap tmB1, I8Shape s) {
+  static_assert(CLP == 1 || CLP == 2, "pairs per cluster");
+  using Cfg = I8Cfg2<S, BKB>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr int R0 = 128 / CLP, R1 = Cfg::NC1 / CLP;  // slab rows this CTA fetches per chunk
+  constexpr uint16_t ALL = (uint16_t)((1u << (2 * CLP)) - 1);
+  constexpr int NC1 = Cfg::NC1;
+  constexpr int A_BYTES = I8_BM * BKB;          // this CTA's 128 rows
+  constexpr int BH_BYTES = Cfg::BH_ROWS * BKB;  // this CTA's halves of the two N chunks
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = sA + I8_STAGES2 * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + I8_STAGES2 * BH_BYTES);
-  uint64_t* empty = full + I8_STAGES2;
-  uint64_t* tmem_full = empty + I8_STAGES2;
+  uint8_t* sB = sA + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * BH_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   I8EpiSmem* esm = reinterpret_cast<I8EpiSmem*>(tmem_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) i8_stamp(s, 0);
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u, pq = crank >> 1;  // role in the pair, pair index in the cluster
   const bool leader = rank == 0;
   int tm, tn;
   {
-    const int pid = blockIdx.x / 2;
-    const int tiles_mc = s.tiles_m / 2;
-    const int gm = max(1, s.group_m / 2);
+    const int pid = blockIdx.x / (2 * CLP);
+    const int tiles_mc = s.tiles_m / (2 * CLP);
+    const int gm = max(1, s.group_m / (2 * CLP));
     const int per_group = gm * s.tiles_n;
     const int g = pid / per_group;
     const int first_m = g * gm;
     const int gsz = min(tiles_mc - first_m, gm);
     const int r = pid - g * per_group;
-    tm = (first_m + r % gsz) * 2 + (int)rank;
+    tm = (first_m + r % gsz) * (2 * CLP) + (int)crank;
     tn = r / gsz;
   }
   const int m0 = tm * I8_BM;
-  const int brow0 = tn * I8_BROWS;
+  const int brow0 = tn * S * I8_NB;
   const int k_end = tn < s.tri_tiles ? min(s.K, (tn + 1) * I8_NB) : s.K;
-  const int KB = (k_end + I8_BKB - 1) / I8_BKB;
+  const int KB = (k_end + BKB - 1) / BKB;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < I8_STAGES2; ++i) {
+    for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], CLP);
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -508,53 +551,60 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB1)) : "memory");
       unsigned long long wprod = 0;
       for (int kb = 0; kb < KB; ++kb) {
-        const int st = kb % I8_STAGES2;
-        if (kb >= I8_STAGES2) {
+        const int st = kb % STAGES;
+        if (kb >= STAGES) {
           const long long c0 = s.trace ? clock64() : 0;
-          mbar_wait(&empty[st], ((kb / I8_STAGES2) - 1) & 1);
+          mbar_wait(&empty[st], ((kb / STAGES) - 1) & 1);
           if (s.trace) wprod += clock64() - c0;
         }
         if (leader) mbar_expect_tx(&full[st], 2 * (A_BYTES + BH_BYTES));  // both CTAs' bytes land on it
-        tma_load_2d_2sm(sA + st * A_BYTES, &tmA, &full[st], kb * I8_BKB, m0);
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d_2sm(sB + st * BH_BYTES + c * 128 * I8_BKB, &tmB, &full[st], kb * I8_BKB,
-                          brow0 + c * 256 + (int)rank * 128);
+        tma_load_2d_2sm(sA + st * A_BYTES, &tmA, &full[st], kb * BKB, m0);
+        if constexpr (CLP == 1) {
+          tma_load_2d_2sm(sB + st * BH_BYTES, &tmB, &full[st], kb * BKB, brow0 + (int)rank * 128);
+          tma_load_2d_2sm(sB + st * BH_BYTES + 128 * BKB, &tmB1, &full[st], kb * BKB, brow0 + 256 + (int)rank * NC1);
+        } else {
+          const uint16_t mc = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // role `rank` of both pairs
+          tma_load_2d_2sm_mc(sB + st * BH_BYTES + pq * R0 * BKB, &tmB, &full[st], kb * BKB,
+                             brow0 + (int)rank * 128 + (int)pq * R0, mc);
+          tma_load_2d_2sm_mc(sB + st * BH_BYTES + (128 + pq * R1) * BKB, &tmB1, &full[st], kb * BKB,
+                             brow0 + 256 + (int)rank * NC1 + (int)pq * R1, mc);
+        }
       }
       i8_put(s, 9, wprod);
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = idesc_i8_m256(256);
+      constexpr uint32_t idesc0 = idesc_i8_m256(256);      // digits 0..3
+      constexpr uint32_t idesc1 = idesc_i8_m256(2 * NC1);  // digits 4..S-1
       unsigned long long wmma = 0;
       for (int kb = 0; kb < KB; ++kb) {
-        const int st = kb % I8_STAGES2;
+        const int st = kb % STAGES;
         const long long c0 = s.trace ? clock64() : 0;
-        mbar_wait(&full[st], (kb / I8_STAGES2) & 1);
+        mbar_wait(&full[st], (kb / STAGES) & 1);
         if (s.trace && kb > 0) wmma += clock64() - c0;
         if (kb == 0) i8_stamp(s, 2);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t a0 = smem_u32(sA + st * A_BYTES);
         const uint32_t b0 = smem_u32(sB + st * BH_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < I8_BKB / 32; ++kk) {
-          const uint64_t ad = umma_desc_sw64(a0 + kk * 32);
+        for (int kk = 0; kk < BKB / 32; ++kk) {
+          const uint64_t ad = umma_desc_k<BKB>(a0 + kk * 32);
           const uint32_t acc = (kb | kk) ? 1u : 0u;
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-            umma_i8_2sm(tmem_base + c * 256, ad, umma_desc_sw64(b0 + c * 128 * I8_BKB + kk * 32), idesc, acc);
+          umma_i8_2sm(tmem_base, ad, umma_desc_k<BKB>(b0 + kk * 32), idesc0, acc);
+          umma_i8_2sm(tmem_base + 256, ad, umma_desc_k<BKB>(b0 + 128 * BKB + kk * 32), idesc1, acc);
         }
-        umma_commit_2sm(&empty[st]);  // both CTAs may refill this stage once these MMAs have read it
+        umma_commit_2sm(&empty[st], ALL);  // every CTA may refill this stage once all pairs' MMAs have read it
       }
-      umma_commit_2sm(tmem_full);
+      umma_commit_2sm(tmem_full, (uint16_t)(3u << (2 * pq)));  // this pair's accumulators complete
       i8_stamp(s, 3);
       i8_put(s, 8, wmma);
       i8_put(s, 10, KB);
     }
   } else if (warp >= 4) {
-    i8_epilogue<I8_SLICES>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
+    i8_epilogue<S>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
     if (threadIdx.x == 128) i8_stamp(s, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

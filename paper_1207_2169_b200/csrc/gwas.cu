@@ -705,17 +705,17 @@ gwas_status launch_schur(const gw::SchurArgs& a, int p, cudaStream_t st) {
 }
 
 // K1i/K2a: C_a[i][c] (c < na) and C_b[i][c'] (c' < nb) from the u8 A block and the stacked digit matrix.
-// Launch of the S-digit kernel with cluster size CL (1 = plain launch).
-template <int S>
+// Launch of the S-digit kernel with cluster size CL (1 = plain launch) and BKB-byte K stages.
+template <int S, int BKB>
 gwas_status launch_i8_s(int CL, const CUtensorMap& ma, const CUtensorMap& mb, const gw::I8Shape& s, unsigned grid,
                         cudaStream_t st) {
-  constexpr size_t smem = gw::I8Cfg<S>::smem_bytes(gw::I8_EPI_SMEM);
+  constexpr size_t smem = gw::I8Cfg<S, BKB>::smem_bytes(gw::I8_EPI_SMEM);
   static std::atomic<uint64_t> attr1{0}, attr2{0}, attr4{0};
-  CKG(ensure_smem_attr(gw::gemm_i8_sliced<1, S>, smem, attr1));
-  CKG(ensure_smem_attr(gw::gemm_i8_sliced<2, S>, smem, attr2));
-  CKG(ensure_smem_attr(gw::gemm_i8_sliced<4, S>, smem, attr4));
+  CKG(ensure_smem_attr(gw::gemm_i8_sliced<1, S, BKB>, smem, attr1));
+  CKG(ensure_smem_attr(gw::gemm_i8_sliced<2, S, BKB>, smem, attr2));
+  CKG(ensure_smem_attr(gw::gemm_i8_sliced<4, S, BKB>, smem, attr4));
   if (CL == 1) {
-    gw::gemm_i8_sliced<1, S><<<grid, gw::I8_THREADS, smem, st>>>(ma, mb, s);
+    gw::gemm_i8_sliced<1, S, BKB><<<grid, gw::I8_THREADS, smem, st>>>(ma, mb, s);
     CKC(cudaGetLastError());
     return GWAS_OK;
   }
@@ -731,8 +731,31 @@ gwas_status launch_i8_s(int CL, const CUtensorMap& ma, const CUtensorMap& mb, co
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (CL == 2) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<2, S>, ma, mb, s));
-  else CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4, S>, ma, mb, s));
+  if (CL == 2) CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<2, S, BKB>, ma, mb, s));
+  else CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced<4, S, BKB>, ma, mb, s));
+  return GWAS_OK;
+}
+
+// The 2-SM kernel (CTA pairs, cta_group::2 MMAs of M = 256), CLP pairs per cluster.
+template <int S, int BKB, int CLP>
+gwas_status launch_i8_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mb1,
+                          const gw::I8Shape& s, unsigned grid, cudaStream_t st) {
+  constexpr size_t smem = gw::I8Cfg2<S, BKB>::smem_bytes(gw::I8_EPI_SMEM);
+  static std::atomic<uint64_t> attr{0};
+  CKG(ensure_smem_attr(gw::gemm_i8_sliced_2sm<S, BKB, CLP>, smem, attr));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(gw::I8_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 2 * CLP;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced_2sm<S, BKB, CLP>, ma, mb, mb1, s));
   return GWAS_OK;
 }
 
@@ -743,25 +766,39 @@ gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, c
                       int64_t fP_stride = 0) {
   if (M <= 0) return GWAS_OK;
   if (S != 7 && S != 8) return fail(GWAS_E_ARG, "int8 digits %d", S);
-  // GWAS_I8_KERNEL: "1sm" (default) with GWAS_I8_CLUSTER (1, 2 or 4; default 2) CTAs multicasting the digit
-  // slab, or "2sm" (CTA pairs with cta_group::2 MMAs).  Measured at C4 per 8192-column block: 1sm x1 14.4 ms,
-  // x2 8.8 ms, x4 9.9 ms; 2sm 9.4 ms.
+  // Kernel choice (measured at C4, 7 digits, K1i per 8192-SNP block, profiles/ncu_int8_c4_r02.md):
+  //   2-SM pairs, 128-byte K stages (default when the block has > 128 rows)      5.42 ms
+  //   2-SM, two pairs per cluster sharing the slab (GWAS_I8_CLUSTER=4)           5.56 ms
+  //   1-SM, 2-CTA slab multicast, 128-byte / 64-byte K stages (GWAS_I8_KERNEL=1sm) 6.19 / 6.94 ms
+  //   2-SM, 64-byte K stages (GWAS_I8_BK=64)                                     7.87 ms
+  // GWAS_I8_KERNEL=1sm|2sm, GWAS_I8_CLUSTER=1|2|4 and GWAS_I8_BK=64|128 override the choice (tests, tuning).
   static int mode_env = [] {
     const char* e = getenv("GWAS_I8_KERNEL");
-    return (e && std::string(e) == "2sm") ? 2 : 1;
+    return (e && std::string(e) == "1sm") ? 1 : 2;
   }();
   static int cl_env = [] {
     const char* e = getenv("GWAS_I8_CLUSTER");
     const int v = e ? atoi(e) : 2;
     return (v == 1 || v == 2 || v == 4) ? v : 2;
   }();
-  const bool two_sm = mode_env == 2 && M > gw::I8_BM && S == gw::I8_SLICES;
-  const int CL = two_sm ? 2 : ((M >= (int64_t)cl_env * gw::I8_BM) ? cl_env : 1);
+  static int bk_env = [] {
+    const char* e = getenv("GWAS_I8_BK");
+    return e ? (atoi(e) == 64 ? 64 : 128) : 0;
+  }();
+  const bool two_sm = mode_env == 2 && M > gw::I8_BM;
+  // 2-SM: cluster of 4 (two pairs sharing the slab) only on request and when the block has > 2 row tiles
+  const int CL = two_sm ? ((cl_env == 4 && M > 2 * gw::I8_BM) ? 4 : 2)
+                        : ((M >= (int64_t)cl_env * gw::I8_BM) ? cl_env : 1);
+  const int CLP = two_sm ? CL / 2 : 1;
+  // 128-byte stages except the 1-SM 8-digit kernel, whose 80 KB stages would leave a 2-deep ring (8.94 vs 7.57 ms)
+  const int bk = bk_env ? bk_env : (!two_sm && S == 8 ? 64 : 128);
   const int brows = S * gw::I8_NB;  // digit rows per 64-column tile
-  CUtensorMap ma, mb;
-  CKG(make_map(&ma, A, true, K, M, lda, gw::I8_BM, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
-  const int box_b = two_sm ? 128 : (CL == 1 ? brows / 2 : brows / CL);
-  CKG(make_map(&mb, dig, true, K, tiles_n * brows, ldd, box_b, gw::I8_BKB, CU_TENSOR_MAP_SWIZZLE_64B));
+  const int swz = bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUtensorMap ma, mb, mb1;
+  CKG(make_map(&ma, A, true, K, M, lda, gw::I8_BM, bk, swz));
+  const int box_b = two_sm ? 128 / CLP : (CL == 1 ? brows / 2 : brows / CL);
+  CKG(make_map(&mb, dig, true, K, tiles_n * brows, ldd, box_b, bk, swz));
+  if (two_sm) CKG(make_map(&mb1, dig, true, K, tiles_n * brows, ldd, (S - 4) * 32 / CLP, bk, swz));
   gw::I8Shape s;
   s.M = (int)M;
   s.K = (int)K;
@@ -798,27 +835,15 @@ gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, c
   s.fP_stride = fP_stride;
   const unsigned grid = (unsigned)(s.tiles_m * s.tiles_n);
   if (two_sm) {
-    constexpr size_t smem2 =
-        1024 + gw::I8_STAGES2 * (gw::I8_BM + gw::I8_BROWS / 2) * gw::I8_BKB + 256 + gw::I8_EPI_SMEM;
-    static std::atomic<uint64_t> attr_2sm{0};
-    CKG(ensure_smem_attr(gw::gemm_i8_sliced_2sm, smem2, attr_2sm));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(gw::I8_THREADS);
-    cfg.dynamicSmemBytes = smem2;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced_2sm, ma, mb, s));
+    auto f = S == 8 ? (bk == 128 ? (CLP == 2 ? launch_i8_2sm<8, 128, 2> : launch_i8_2sm<8, 128, 1>)
+                                 : (CLP == 2 ? launch_i8_2sm<8, 64, 2> : launch_i8_2sm<8, 64, 1>))
+                    : (bk == 128 ? (CLP == 2 ? launch_i8_2sm<7, 128, 2> : launch_i8_2sm<7, 128, 1>)
+                                 : (CLP == 2 ? launch_i8_2sm<7, 64, 2> : launch_i8_2sm<7, 64, 1>));
+    CKG(f(ma, mb, mb1, s, grid, st));
   } else if (S == 8) {
-    CKG(launch_i8_s<8>(CL, ma, mb, s, grid, st));
+    CKG((bk == 128 ? launch_i8_s<8, 128>(CL, ma, mb, s, grid, st) : launch_i8_s<8, 64>(CL, ma, mb, s, grid, st)));
   } else {
-    CKG(launch_i8_s<7>(CL, ma, mb, s, grid, st));
+    CKG((bk == 128 ? launch_i8_s<7, 128>(CL, ma, mb, s, grid, st) : launch_i8_s<7, 64>(CL, ma, mb, s, grid, st)));
   }
   CKC(cudaGetLastError());
   if (trace_dev) {

@@ -376,8 +376,8 @@ def test_no_writes_outside_caller_buffers(i8, ovl, mode):
 
 @pytest.mark.parametrize("S", [8, 7])
 def test_int8_sliced_kernel_variants_agree(c0, S):
-    """The 1-SM (cluster 1, 2, 4) and 2-SM (cta_group::2, S = 8 only) int8 kernels give bitwise identical results
-    (the int32 digit products are exact, the fp64 recombination is the same code)."""
+    """The 1-SM (cluster 1, 2, 4) and 2-SM (cta_group::2) int8 kernels, with 64- or 128-byte K stages, give bitwise
+    identical results (the int32 digit products are exact, the fp64 recombination is the same code)."""
     import os
     import subprocess
     import sys
@@ -391,10 +391,10 @@ def test_int8_sliced_kernel_variants_agree(c0, S):
     outs = []
     import tempfile
     with tempfile.TemporaryDirectory() as d:
-        variants = (("1sm", "1"), ("1sm", "2"), ("1sm", "4")) + ((("2sm", "2"),) if S == 8 else ())
-        for i, (kern, cl) in enumerate(variants):
+        variants = [(k, cl, bk) for bk in ("128", "64") for k, cl in (("1sm", "1"), ("1sm", "2"), ("1sm", "4"), ("2sm", "2"), ("2sm", "4"))]
+        for i, (kern, cl, bk) in enumerate(variants):
             f = os.path.join(d, f"r{i}.npy")
-            env = dict(os.environ, GWAS_I8_KERNEL=kern, GWAS_I8_CLUSTER=cl)
+            env = dict(os.environ, GWAS_I8_KERNEL=kern, GWAS_I8_CLUSTER=cl, GWAS_I8_BK=bk)
             subprocess.run([sys.executable, "-c", code, f], check=True, env=env, cwd=os.path.dirname(os.path.dirname(__file__)))
             outs.append(np.load(f))
     for o in outs[1:]:
