@@ -146,6 +146,16 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// Address of the same shared-memory variable in CTA `rank` of the cluster, and a release arrive on it.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -195,11 +205,12 @@ constexpr int I8_EPI_SMEM = (int)sizeof(I8EpiSmem);
 
 template <int S>
 __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base, uint64_t* tmem_full, int m0, int tn,
-                                            int warp, int lane, I8EpiSmem* es) {
+                                            int warp, int lane, I8EpiSmem* es, uint32_t parity = 0) {
   // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = tile rows
   const int q = warp & 3;
   const int row = m0 + q * 32 + lane;
   {
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");  // (persistent CTAs) the previous tile's reads of es are done
     const int et = threadIdx.x - 128;  // 0..127 over the four epilogue warps
     const int oc = tn * I8_NB;
     if (et < I8_NB) es->scale[et] = scalbn(1.0, __ldg(s.exps + oc + et) - 28);
@@ -210,7 +221,7 @@ __device__ __forceinline__ void i8_epilogue(const I8Shape& s, uint32_t tmem_base
       }
     asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the four epilogue warps only
   }
-  mbar_wait(tmem_full, 0);
+  mbar_wait(tmem_full, parity);
   if (threadIdx.x == 128) i8_stamp(s, 4);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
@@ -494,6 +505,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   constexpr int NC1 = Cfg::NC1;
   constexpr int A_BYTES = I8_BM * BKB;          // this CTA's 128 rows
   constexpr int BH_BYTES = Cfg::BH_ROWS * BKB;  // this CTA's halves of the two N chunks
+  static_assert((2 * STAGES + 4) * 8 <= 256, "barriers + TMEM slot exceed their 256-byte region");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -501,17 +513,20 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * BH_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  I8EpiSmem* esm = reinterpret_cast<I8EpiSmem*>(tmem_full + 2);
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  I8EpiSmem* esm = reinterpret_cast<I8EpiSmem*>(tmem_empty + 3);  // 16-byte aligned (double2 loads of es->d)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) i8_stamp(s, 0);
   const uint32_t crank = cluster_ctarank();
   const uint32_t rank = crank & 1u, pq = crank >> 1;  // role in the pair, pair index in the cluster
   const bool leader = rank == 0;
-  int tm, tn;
-  {
-    const int pid = blockIdx.x / (2 * CLP);
+  // Persistent clusters: cluster c computes cluster tiles c, c + nclu, ... (grid = every tile: one each).  A cluster
+  // tile is CLP consecutive 256-row pair tiles of one 64-column tile, in grouped rasterisation.
+  const int nclu = (int)gridDim.x / (2 * CLP);
+  const int ctiles = (s.tiles_m / (2 * CLP)) * s.tiles_n;
+  auto tile_of = [&](int pid, int& m0, int& tn, int& KB) {
     const int tiles_mc = s.tiles_m / (2 * CLP);
     const int gm = max(1, s.group_m / (2 * CLP));
     const int per_group = gm * s.tiles_n;
@@ -519,13 +534,11 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     const int first_m = g * gm;
     const int gsz = min(tiles_mc - first_m, gm);
     const int r = pid - g * per_group;
-    tm = (first_m + r % gsz) * (2 * CLP) + (int)crank;
+    m0 = ((first_m + r % gsz) * (2 * CLP) + (int)crank) * I8_BM;
     tn = r / gsz;
-  }
-  const int m0 = tm * I8_BM;
-  const int brow0 = tn * S * I8_NB;
-  const int k_end = tn < s.tri_tiles ? min(s.K, (tn + 1) * I8_NB) : s.K;
-  const int KB = (k_end + BKB - 1) / BKB;
+    const int k_end = tn < s.tri_tiles ? min(s.K, (tn + 1) * I8_NB) : s.K;
+    KB = (k_end + BKB - 1) / BKB;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -533,6 +546,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       mbar_init(&empty[i], CLP);
     }
     mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 8);  // the 4 epilogue warps of both CTAs of the pair (used in the leader)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {  // both CTAs: one warp each, same smem slot
@@ -553,24 +567,30 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB1)) : "memory");
       unsigned long long wprod = 0;
-      for (int kb = 0; kb < KB; ++kb) {
-        const int st = kb % STAGES;
-        if (kb >= STAGES) {
-          const long long c0 = s.trace ? clock64() : 0;
-          mbar_wait(&empty[st], ((kb / STAGES) - 1) & 1);
-          if (s.trace) wprod += clock64() - c0;
-        }
-        if (leader) mbar_expect_tx(&full[st], 2 * (A_BYTES + BH_BYTES));  // both CTAs' bytes land on it
-        tma_load_2d_2sm(sA + st * A_BYTES, &tmA, &full[st], kb * BKB, m0);
-        if constexpr (CLP == 1) {
-          tma_load_2d_2sm(sB + st * BH_BYTES, &tmB, &full[st], kb * BKB, brow0 + (int)rank * 128);
-          tma_load_2d_2sm(sB + st * BH_BYTES + 128 * BKB, &tmB1, &full[st], kb * BKB, brow0 + 256 + (int)rank * NC1);
-        } else {
-          const uint16_t mc = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // role `rank` of both pairs
-          tma_load_2d_2sm_mc(sB + st * BH_BYTES + pq * R0 * BKB, &tmB, &full[st], kb * BKB,
-                             brow0 + (int)rank * 128 + (int)pq * R0, mc);
-          tma_load_2d_2sm_mc(sB + st * BH_BYTES + (128 + pq * R1) * BKB, &tmB1, &full[st], kb * BKB,
-                             brow0 + 256 + (int)rank * NC1 + (int)pq * R1, mc);
+      int gk = 0;  // stage counter across this cluster's tiles (the ring runs on into the next tile)
+      for (int pid = (int)blockIdx.x / (2 * CLP); pid < ctiles; pid += nclu) {
+        int m0, tn, KB;
+        tile_of(pid, m0, tn, KB);
+        const int brow0 = tn * S * I8_NB;
+        for (int kb = 0; kb < KB; ++kb, ++gk) {
+          const int st = gk % STAGES;
+          if (gk >= STAGES) {
+            const long long c0 = s.trace ? clock64() : 0;
+            mbar_wait(&empty[st], ((gk / STAGES) - 1) & 1);
+            if (s.trace) wprod += clock64() - c0;
+          }
+          if (leader) mbar_expect_tx(&full[st], 2 * (A_BYTES + BH_BYTES));  // both CTAs' bytes land on it
+          tma_load_2d_2sm(sA + st * A_BYTES, &tmA, &full[st], kb * BKB, m0);
+          if constexpr (CLP == 1) {
+            tma_load_2d_2sm(sB + st * BH_BYTES, &tmB, &full[st], kb * BKB, brow0 + (int)rank * 128);
+            tma_load_2d_2sm(sB + st * BH_BYTES + 128 * BKB, &tmB1, &full[st], kb * BKB, brow0 + 256 + (int)rank * NC1);
+          } else {
+            const uint16_t mc = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // role `rank` of both pairs
+            tma_load_2d_2sm_mc(sB + st * BH_BYTES + pq * R0 * BKB, &tmB, &full[st], kb * BKB,
+                               brow0 + (int)rank * 128 + (int)pq * R0, mc);
+            tma_load_2d_2sm_mc(sB + st * BH_BYTES + (128 + pq * R1) * BKB, &tmB1, &full[st], kb * BKB,
+                               brow0 + 256 + (int)rank * NC1 + (int)pq * R1, mc);
+          }
         }
       }
       i8_put(s, 9, wprod);
@@ -580,31 +600,50 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
       constexpr uint32_t idesc0 = idesc_i8_m256(256);      // digits 0..3
       constexpr uint32_t idesc1 = idesc_i8_m256(2 * NC1);  // digits 4..S-1
       unsigned long long wmma = 0;
-      for (int kb = 0; kb < KB; ++kb) {
-        const int st = kb % STAGES;
-        const long long c0 = s.trace ? clock64() : 0;
-        mbar_wait(&full[st], (kb / STAGES) & 1);
-        if (s.trace && kb > 0) wmma += clock64() - c0;
-        if (kb == 0) i8_stamp(s, 2);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t a0 = smem_u32(sA + st * A_BYTES);
-        const uint32_t b0 = smem_u32(sB + st * BH_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < BKB / 32; ++kk) {
-          const uint64_t ad = umma_desc_k<BKB>(a0 + kk * 32);
-          const uint32_t acc = (kb | kk) ? 1u : 0u;
-          umma_i8_2sm(tmem_base, ad, umma_desc_k<BKB>(b0 + kk * 32), idesc0, acc);
-          umma_i8_2sm(tmem_base + 256, ad, umma_desc_k<BKB>(b0 + 128 * BKB + kk * 32), idesc1, acc);
+      int gk = 0, it = 0;
+      for (int pid = (int)blockIdx.x / (2 * CLP); pid < ctiles; pid += nclu, ++it) {
+        int m0, tn, KB;
+        tile_of(pid, m0, tn, KB);
+        if (it > 0) {  // the previous tile's accumulators drained by both CTAs' epilogues
+          mbar_wait(tmem_empty, (it - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         }
-        umma_commit_2sm(&empty[st], ALL);  // every CTA may refill this stage once all pairs' MMAs have read it
+        for (int kb = 0; kb < KB; ++kb, ++gk) {
+          const int st = gk % STAGES;
+          const long long c0 = s.trace ? clock64() : 0;
+          mbar_wait(&full[st], (gk / STAGES) & 1);
+          if (s.trace && gk > 0) wmma += clock64() - c0;
+          if (gk == 0) i8_stamp(s, 2);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + st * A_BYTES);
+          const uint32_t b0 = smem_u32(sB + st * BH_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BKB / 32; ++kk) {
+            const uint64_t ad = umma_desc_k<BKB>(a0 + kk * 32);
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            umma_i8_2sm(tmem_base, ad, umma_desc_k<BKB>(b0 + kk * 32), idesc0, acc);
+            umma_i8_2sm(tmem_base + 256, ad, umma_desc_k<BKB>(b0 + 128 * BKB + kk * 32), idesc1, acc);
+          }
+          umma_commit_2sm(&empty[st], ALL);  // every CTA may refill this stage once all pairs' MMAs have read it
+        }
+        umma_commit_2sm(tmem_full, (uint16_t)(3u << (2 * pq)));  // this pair's accumulators complete
       }
-      umma_commit_2sm(tmem_full, (uint16_t)(3u << (2 * pq)));  // this pair's accumulators complete
       i8_stamp(s, 3);
       i8_put(s, 8, wmma);
-      i8_put(s, 10, KB);
+      i8_put(s, 10, gk);
     }
   } else if (warp >= 4) {
-    i8_epilogue<S>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm);
+    // TMEM drained -> the pair leader's tmem_empty (remote arrive from the peer CTA)
+    const uint32_t empty_leader = mapa_shared(smem_u32(tmem_empty), crank & ~1u);
+    int it = 0;
+    for (int pid = (int)blockIdx.x / (2 * CLP); pid < ctiles; pid += nclu, ++it) {
+      int m0, tn, KB;
+      tile_of(pid, m0, tn, KB);
+      i8_epilogue<S>(s, tmem_base, tmem_full, m0, tn, warp, lane, esm, (uint32_t)(it & 1));
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(empty_leader);
+    }
     if (threadIdx.x == 128) i8_stamp(s, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

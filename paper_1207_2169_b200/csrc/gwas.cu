@@ -755,6 +755,15 @@ gwas_status launch_i8_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   la[0].val.clusterDim.z = 1;
   cfg.attrs = la;
   cfg.numAttrs = 1;
+  // Persistent clusters (GWAS_I8_PERSIST=0: one cluster per cluster tile): as many as can be co-resident, each
+  // looping over cluster tiles, so a tile's first stages load while the previous tile's accumulators drain.
+  static const int persist = getenv("GWAS_I8_PERSIST") ? atoi(getenv("GWAS_I8_PERSIST")) : 1;
+  if (persist) {
+    int nclu = 0;  // per call: cheap beside a multi-ms launch, and correct for whichever device is current
+    CKC(cudaOccupancyMaxActiveClusters(&nclu, gw::gemm_i8_sliced_2sm<S, BKB, CLP>, &cfg));
+    const unsigned ctiles = grid / (2 * CLP);
+    if (nclu > 0 && (unsigned)nclu < ctiles) cfg.gridDim = dim3((unsigned)nclu * 2 * CLP);
+  }
   CKC(cudaLaunchKernelEx(&cfg, gw::gemm_i8_sliced_2sm<S, BKB, CLP>, ma, mb, mb1, s));
   return GWAS_OK;
 }
@@ -766,29 +775,33 @@ gwas_status launch_i8(int S, const void* A, int64_t lda, int64_t M, int64_t K, c
                       int64_t fP_stride = 0) {
   if (M <= 0) return GWAS_OK;
   if (S != 7 && S != 8) return fail(GWAS_E_ARG, "int8 digits %d", S);
-  // Kernel choice (measured at C4, 7 digits, K1i per 8192-SNP block, profiles/ncu_int8_c4_r02.md):
-  //   2-SM pairs, 128-byte K stages (default when the block has > 128 rows)      5.42 ms
-  //   2-SM, two pairs per cluster sharing the slab (GWAS_I8_CLUSTER=4)           5.56 ms
-  //   1-SM, 2-CTA slab multicast, 128-byte / 64-byte K stages (GWAS_I8_KERNEL=1sm) 6.19 / 6.94 ms
-  //   2-SM, 64-byte K stages (GWAS_I8_BK=64)                                     7.87 ms
-  // GWAS_I8_KERNEL=1sm|2sm, GWAS_I8_CLUSTER=1|2|4 and GWAS_I8_BK=64|128 override the choice (tests, tuning).
+  // Kernel choice (measured at C4, K1i per 8192-SNP block, 5 passes; profiles/ncu_int8_c4_r02.md):
+  //                                                        7 digits   8 digits
+  //   2-SM pairs, 128-byte K stages, persistent clusters:
+  //     two pairs per cluster sharing the slab              5.39 ms    6.04 ms   (7-digit default)
+  //     one pair per cluster                                5.48 ms    5.91 ms   (8-digit default)
+  //   the same, one cluster per tile (GWAS_I8_PERSIST=0)    5.60/5.43  6.26/5.99
+  //   2-SM, 64-byte K stages (GWAS_I8_BK=64)                7.87 ms    8.47 ms
+  //   1-SM, 2-CTA slab multicast, 128/64-byte stages        6.19/6.94  8.94/7.57 (used when the block has <= 128 rows)
+  // GWAS_I8_KERNEL=1sm|2sm, GWAS_I8_CLUSTER=1|2|4, GWAS_I8_BK=64|128 and GWAS_I8_PERSIST=0|1 override the choice.
   static int mode_env = [] {
     const char* e = getenv("GWAS_I8_KERNEL");
     return (e && std::string(e) == "1sm") ? 1 : 2;
   }();
   static int cl_env = [] {
     const char* e = getenv("GWAS_I8_CLUSTER");
-    const int v = e ? atoi(e) : 2;
-    return (v == 1 || v == 2 || v == 4) ? v : 2;
+    const int v = e ? atoi(e) : 0;
+    return (v == 1 || v == 2 || v == 4) ? v : 0;
   }();
   static int bk_env = [] {
     const char* e = getenv("GWAS_I8_BK");
     return e ? (atoi(e) == 64 ? 64 : 128) : 0;
   }();
   const bool two_sm = mode_env == 2 && M > gw::I8_BM;
-  // 2-SM: cluster of 4 (two pairs sharing the slab) only on request and when the block has > 2 row tiles
-  const int CL = two_sm ? ((cl_env == 4 && M > 2 * gw::I8_BM) ? 4 : 2)
-                        : ((M >= (int64_t)cl_env * gw::I8_BM) ? cl_env : 1);
+  const int cl_want = cl_env ? cl_env : (two_sm ? (S == 7 ? 4 : 2) : 2);
+  // 2-SM: a cluster of 4 (two pairs sharing the slab) needs more than two row tiles
+  const int CL = two_sm ? ((cl_want == 4 && M > 2 * gw::I8_BM) ? 4 : 2)
+                        : ((M >= (int64_t)cl_want * gw::I8_BM) ? cl_want : 1);
   const int CLP = two_sm ? CL / 2 : 1;
   // 128-byte stages except the 1-SM 8-digit kernel, whose 80 KB stages would leave a 2-deep ring (8.94 vs 7.57 ms)
   const int bk = bk_env ? bk_env : (!two_sm && S == 8 ? 64 : 128);
