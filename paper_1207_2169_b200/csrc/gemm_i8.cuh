@@ -14,12 +14,15 @@
 // i.e. B = B_lin = Z B_op (precomputed once in setup).  Both share the A operand, so one launch covers both:
 // output tiles [0, na_tiles) write C_a (X_R'^T), the rest write C_b (the linear block of the K2 output).
 //
-// Kernel: one 128 x 64 output tile per CTA.  B rows of a tile are stacked digit-major (row s*64 + j = digit s
-// of output column j), so the S*64 (512 or 448) int32 accumulators of the tile fit TMEM's 512 columns x 128
-// lanes.  Warp 0: TMA producer (A box 64 B x 128 rows, B boxes of the S*64-row digit slab, 64-byte swizzle,
-// multicast across a 2-CTA cluster) into a STAGES ring; warp 1: TMEM allocation + single-thread tcgen05.mma issue
-// (M = 128, N = 256 and N = (S-4)*64, K = 32 per instruction), tcgen05.commit -> mbarriers; warps 4-7: epilogue
-// (tcgen05.ld 32x32b, exact int64 recombination, fp64 stores or the fused squared-term partials).
+// Tiles: 128 SNP rows x 64 output columns per CTA.  B rows of a tile are stacked digit-major (row s*64 + j = digit
+// s of output column j), so the S*64 (512 or 448) int32 accumulators of the tile fit TMEM's 512 columns x 128
+// lanes.  Warp 0: TMA producer into a STAGES ring of BKB-byte K stages; warp 1: TMEM allocation + single-thread
+// tcgen05.mma issue (N = 256 for digits 0..3 and N = (S-4)*64 for the rest, K = 32 per instruction),
+// tcgen05.commit -> mbarriers; warps 4-7: epilogue (tcgen05.ld 32x32b, exact int64 recombination, fp64 stores or
+// the fused squared-term partials).  Two kernels:
+//   gemm_i8_sliced_2sm (default): CTA pairs issue cta_group::2 MMAs (M = 256), each CTA staging its 128 A rows and
+//     half of the slab, persistent clusters of one or two pairs, 128-byte K stages (128-byte swizzle);
+//   gemm_i8_sliced: 1-SM MMAs (M = 128), 2- or 4-CTA clusters multicasting the slab (blocks of <= 128 rows).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
