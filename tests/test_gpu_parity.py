@@ -376,25 +376,29 @@ def test_no_writes_outside_caller_buffers(i8, ovl, mode):
 
 @pytest.mark.parametrize("S", [8, 7])
 def test_int8_sliced_kernel_variants_agree(c0, S):
-    """The 1-SM (cluster 1, 2, 4) and 2-SM (cta_group::2) int8 kernels, with 64- or 128-byte K stages, give bitwise
-    identical results (the int32 digit products are exact, the fp64 recombination is the same code)."""
+    """The 1-SM (cluster 1, 2, 4) and 2-SM (cta_group::2; one or two pairs per cluster, persistent or not) int8
+    kernels, with 64- or 128-byte K stages, give bitwise identical results (the int32 digit products are exact, the
+    fp64 recombination is the same code)."""
     import os
     import subprocess
     import sys
     code = ("import sys, numpy as np, torch, datagen; sys.path.insert(0, 'tests');"
             "import paper_1207_2169_b200 as gw;"
-            "cfg = datagen.custom_config(n=333, p=3, m=2000, t=37, index=601); ds = datagen.dataset(cfg);"
+            "cfg = datagen.custom_config(n=333, p=3, m=5000, t=37, index=601); ds = datagen.dataset(cfg);"
             "X = torch.from_numpy(datagen.xr_dosages(cfg, ld=336)).cuda();"
-            f"e = gw.Gwas(cfg.n, cfg.p, cfg.t, int8_slices={S}, block_cols=1024); e.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2);"
+            f"e = gw.Gwas(cfg.n, cfg.p, cfg.t, int8_slices={S}, block_cols=4096); e.setup(ds.Phi, ds.XL, ds.Y, ds.h2, ds.s2);"
             "b, v, s = e.run(X); torch.cuda.synchronize();"
             "np.save(sys.argv[1], np.stack([b.cpu().numpy(), v.cpu().numpy()]))")
     outs = []
     import tempfile
     with tempfile.TemporaryDirectory() as d:
-        variants = [(k, cl, bk) for bk in ("128", "64") for k, cl in (("1sm", "1"), ("1sm", "2"), ("1sm", "4"), ("2sm", "2"), ("2sm", "4"))]
-        for i, (kern, cl, bk) in enumerate(variants):
+        # the 4096-row block has 16 x 9 pair tiles (8 x 9 two-pair tiles), more than the co-resident clusters, so the
+        # persistent 2-SM kernel loops over several tiles per cluster; persist 0 = one cluster per tile
+        variants = [(k, cl, bk, ps) for bk in ("128", "64") for k, cl in (("1sm", "1"), ("1sm", "2"), ("1sm", "4"),
+                    ("2sm", "2"), ("2sm", "4")) for ps in ("1", "0") if k == "2sm" or ps == "1"]
+        for i, (kern, cl, bk, ps) in enumerate(variants):
             f = os.path.join(d, f"r{i}.npy")
-            env = dict(os.environ, GWAS_I8_KERNEL=kern, GWAS_I8_CLUSTER=cl, GWAS_I8_BK=bk)
+            env = dict(os.environ, GWAS_I8_KERNEL=kern, GWAS_I8_CLUSTER=cl, GWAS_I8_BK=bk, GWAS_I8_PERSIST=ps)
             subprocess.run([sys.executable, "-c", code, f], check=True, env=env, cwd=os.path.dirname(os.path.dirname(__file__)))
             outs.append(np.load(f))
     for o in outs[1:]:
