@@ -28,8 +28,13 @@
  *     complement sigma_ij <= eps_collinear * c_ij, reading A6) or 2 (non-finite), with NaN payload.
  */
 /* Environment knobs (tuning / debugging only; results are bitwise unaffected unless stated):
- *   GWAS_I8_CLUSTER=1|2|4   int8 kernel cluster size (digit-slab multicast), default 2
- *   GWAS_I8_KERNEL=2sm      the 2-SM (cta_group::2) int8 kernel, 8 digits only (measured slower; not the default)
+ *   GWAS_I8_KERNEL=1sm      the 1-SM int8 kernel (M = 128 MMAs) for every block; default: the 2-SM (cta_group::2,
+ *                           M = 256) kernel for blocks of more than 128 SNP rows, the 1-SM one otherwise
+ *   GWAS_I8_CLUSTER=1|2|4   int8 cluster size: 1-SM kernel, CTAs multicasting the digit slab (default 2); 2-SM
+ *                           kernel, 2 = one pair, 4 = two pairs sharing the slab (default 4 at 7 digits, 2 at 8)
+ *   GWAS_I8_BK=64|128       int8 K bytes per pipeline stage (64- or 128-byte swizzle); default 128 (64 for the 1-SM
+ *                           8-digit kernel, whose 128-byte stages would leave a 2-deep ring)
+ *   GWAS_I8_PERSIST=0|1     2-SM int8 kernel: persistent clusters looping over tiles (default 1) or one per tile
  *   GWAS_BN64_WAVES=w       force the 128/64-wide tile choice of the DMMA kernel by a w-wave threshold
  *   GWAS_I8_GROUP=g         int8 kernel rasterisation group (row tiles per sweep of the digit slabs), default 32
  *   GWAS_K1_GROUP=g         K1 rasterisation group (row tiles per sweep of the Z panels), default 32
