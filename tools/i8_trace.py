@@ -1,7 +1,9 @@
 """Summarise GWAS_I8_TRACE phase stamps of the int8 kernel (debug).  Usage: python tools/i8_trace.py trace.bin
 Slots per CTA (16): 0 entry, 1 after TMEM alloc + barrier init, 2 first stage landed (MMA thread), 3 last commit
 issued, 4 epilogue sees accumulators, 5 epilogue done, 6 before dealloc, 7 smid, 8 clock64 cycles the MMA thread
-waited on full barriers (after the first stage), 9 cycles the producer waited on empty barriers, 10 k-stages."""
+waited on full barriers (after the first stage), 9 cycles the producer waited on empty barriers, 10 k-stages.
+Persistent 2-SM kernel: slots 2 / 3 bracket ALL of a CTA's tiles and slot 10 counts all its k-stages, so "mainloop
+per k-stage" is the CTA's average stage time with the epilogues included; slot 4 is the last tile's drain start."""
 import sys
 import numpy as np
 a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 4096, 16)
